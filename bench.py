@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Parareal hot path (BASELINE.json metric:
+"Parareal speedup vs serial fine at 1/2/4/8 B200; RHS stencil HBM GB/s vs peak").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3s] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One bench STEP = one complete Parareal solve (pr_parareal: nu tables, coarse
+initial guess, K iterations of fine/coarse/correction with the fused defect,
+NCCL hand-off) of the workload, inputs already resident in HBM.  The workload
+(default cfg3s) is BASELINE configs[2] (256^3, paper-shaped, 1/2/4/8 GPUs)
+shortened 16x in T with the same dt and Dt, N_p = number of GPUs,
+K = min(3, N_p).  `value` is the serial-equivalent fine throughput
+n^3 * N_t / C_p (fine grid-point steps of the serial solution delivered per
+second), so value(N)/value_serial is the Parareal speedup S_measured; the
+serial fine solve is timed in the same run for S_measured and tau_f, and the
+coarse propagator for tau_c (Eq.(speedup)).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synthetic import CONFIGS  # noqa: E402
+
+METRIC = "Parareal speedup vs serial fine at 1/2/4/8 B200; RHS stencil HBM GB/s vs peak"
+UNIT = "fine point-steps/s (serial-equivalent)"
+FINE_BYTES_PER_PT = 128   # one RK4 step, four fused stage passes
+COARSE_BYTES_PER_PT = 16  # one Euler step
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(n):
+    """dram bytes per RK4 step (sum over the 4 stage launches) from the committed
+    ncu --set full summary, if one exists for this grid size."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        v = d.get("fine_step_dram_bytes", {}).get(str(n))
+        return float(v) if v is not None else None
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap",
+              "power.draw"]
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", ",".join(str(g) for g in self.gpus),
+                 "--query-gpu=" + ",".join(self.FIELDS), "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline_sample(cfg, target_s=12.0):
+    """The oracle (plain C, as it stands) on the host cores: serial fine RK4
+    steps of the same grid, the serial-equivalent throughput in `UNIT`."""
+    import oracle
+    oracle.build()
+    n = cfg.n
+    p = oracle.Problem(n, c=cfg.c, nu0=cfg.nu0, omega=cfg.omega, T=cfg.T, nu_mode=cfg.nu_mode)
+    u = oracle.initial(n)
+    dt = cfg.T / cfg.Nt
+    t0 = time.perf_counter()
+    u = oracle.fine(p, u, 0, 1, dt)
+    t1 = time.perf_counter() - t0
+    steps = max(1, min(16, int(target_s / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    oracle.fine(p, u, 1, steps, dt)
+    el = time.perf_counter() - t0
+    return {"value": n ** 3 * steps / el, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
+            "sample": f"{steps} serial fine RK4 steps of the {cfg.name} grid ({n}^3) by oracle/oracle.c "
+                      f"({oracle.threads()} OpenMP threads), {el:.2f} s"}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the oracle timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    n = cfg.n
+    p = oracle.Problem(n, c=cfg.c, nu0=cfg.nu0, omega=cfg.omega, T=cfg.T, nu_mode=cfg.nu_mode)
+    u = oracle.initial(n)
+    dt = cfg.T / cfg.Nt
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        u = oracle.fine(p, u, i, 1, dt)
+        el = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(el)
+    ms = 1e3 * statistics.mean(times)
+    value = n ** 3 / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "n": n, "note": "each step = one serial fine RK4 step "
+                       "of the workload grid by the CPU oracle (a bounded sample of the serial solve)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
+                             "sample": f"{args.steps} timed fine RK4 steps at {n}^3"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg3s")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--K", type=int, default=None, help="override K (default min(3, N_p))")
+    ap.add_argument("--slices", type=int, default=None, help="override N_p (default = world size)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--nu-mode", type=int, default=None)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+    if args.nu_mode is not None:
+        cfg = cfg.with_(nu_mode=args.nu_mode)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1409_8563_b200 as pr
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    n = cfg.n
+    Np = args.slices or world
+    K = args.K if args.K is not None else min(3, Np)
+    nf, nc = cfg.Nt // Np, cfg.NC // Np
+    assert nf * Np == cfg.Nt and nc * Np == cfg.NC, "N_t and N_C must split into N_p slices"
+    problem = pr.Problem(n, c=cfg.c, nu0=cfg.nu0, omega=cfg.omega, T=cfg.T, nu_mode=cfg.nu_mode)
+    grid = pr.Grid(problem, local)
+    if world > 1:
+        pr.comm_init_torch(grid)
+    last = rank == world - 1
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    u0 = torch.empty((n, n, n), dtype=torch.float64, device=dev)
+    pr.pr_fill_sine(grid, u0)
+    uT = torch.empty_like(u0)
+
+    # --- serial fine reference (speedup denominator, u_fine for d^k) and tau_c, on the last rank
+    dt, Dt = cfg.T / cfg.Nt, cfg.T / cfg.NC
+    uref = torch.empty_like(u0) if last else None
+    C_f_ms = tau_f = tau_c = 0.0
+    if last:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        pr.pr_fine(grid, u0, uref, 0, 64, dt)  # warm the graphs and tables
+        pr.pr_coarse(grid, u0, uT, 0, 64, Dt)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        pr.pr_fine(grid, u0, uref, 0, cfg.Nt, dt)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        C_f_ms = e0.elapsed_time(e1)
+        tau_f = C_f_ms / cfg.Nt
+        e0.record(stream)
+        pr.pr_coarse(grid, u0, uT, 0, cfg.NC, Dt)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        tau_c = e0.elapsed_time(e1) / cfg.NC
+    tf_all = max_over_ranks(tau_f)
+    tc_all = max_over_ranks(tau_c)
+    C_f_ms = max_over_ranks(C_f_ms)
+
+    pcfg = pr.PararealCfg(Np, nc, nf, K)
+    for _ in range(args.warmup):
+        pr.pr_parareal(grid, pcfg, u0, uT if last else None, uref)
+    barrier()
+
+    sampler = ClockSampler(list(range(world))) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    l0 = pr.pr_kernel_launches()
+    times, fine_ms, fine_steps = [], 0.0, 0
+    defects = None
+    barrier()
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        d = pr.pr_parareal(grid, pcfg, u0, uT if last else None, uref)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        times.append(e0.elapsed_time(e1))
+        tl = pr.pr_last_timings(grid)
+        fine_ms += tl["fine_ms"]
+        fine_steps += K * (Np // world) * nf
+        if d is not None:
+            defects = d
+    barrier()
+    launches = sum_over_ranks(pr.pr_kernel_launches() - l0)
+    clocks = sampler.stop() if sampler else None
+    ms_per_step = max_over_ranks(sum(times) / len(times))
+    value = n ** 3 * cfg.Nt / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (the fused RK4 stages), measured in the timed region
+    t_fine_step_ms = max_over_ranks(fine_ms / max(fine_steps, 1))
+    achieved = FINE_BYTES_PER_PT * n ** 3 / (t_fine_step_ms / 1e3) / 1e9
+    peak, peak_src = load_peaks()
+    traffic = ncu_traffic(n)
+
+    # e2e: the same solve through the public API with host buffers (pinned), copies timed
+    e2e = None
+    if not args.no_e2e:
+        h_u0 = u0.cpu().pin_memory()
+        h_uT = torch.empty(u0.shape, dtype=torch.float64).pin_memory() if last else None
+        pr.pr_parareal(grid, pcfg, h_u0, h_uT, uref)
+        barrier()
+        et = []
+        for _ in range(max(1, args.steps)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pr.pr_parareal(grid, pcfg, h_u0, h_uT, uref)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            et.append(e0.elapsed_time(e1))
+        barrier()
+        e2e_ms = max_over_ranks(sum(et) / len(et))
+        e2e = {"value": n ** 3 * cfg.Nt / (e2e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": world * 8 * n ** 3,
+               "d2h_bytes_per_step": 8 * n ** 3 + 8 * (K + 1), "ms_per_step": e2e_ms}
+
+    from paper_1409_8563_b200 import perfmodel as pm
+    r = tc_all / tf_all
+    S_meas = C_f_ms / ms_per_step
+    S_bound = pm.speedup_bound(Np, K, nc, nf, tc_all, tf_all)
+    S_ns = pm.speedup_bound_northstar(Np, K, nc, nf, tc_all, tf_all)
+    dlist = None
+    if world > 1:
+        obj = [defects]
+        dist.broadcast_object_list(obj, src=world - 1)
+        dlist = obj[0]
+    else:
+        dlist = defects
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(cfg)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {n}^3 periodic advection-diffusion, T={cfg.T:g}, "
+                                   f"N_t={cfg.Nt}, N_C={cfg.NC}, N_p={Np}, K={K}",
+                       "n": n, "T": cfg.T, "N_t": cfg.Nt, "N_C": cfg.NC, "N_p": Np, "K": K,
+                       "omega": cfg.omega, "nu_mode": ["stage", "step_start"][cfg.nu_mode],
+                       "c": list(cfg.c), "parallelism": f"time-parallel Parareal, {world} GPU(s), "
+                                                        f"{Np // world} slice(s)/GPU",
+                       "l2": "inputs larger than L2 (128 MiB fields at 256^3)" if n >= 256 else
+                             "fields L2-resident"},
+            "speedup": {"S_measured": S_meas, "S_bound_eq_speedup_P229": S_bound,
+                        "frac_of_bound": S_meas / S_bound, "S_bound_northstar_form": S_ns,
+                        "E_measured": S_meas / Np, "E_bound": S_bound / Np,
+                        "C_f_ms": C_f_ms, "C_p_ms": ms_per_step, "tau_f_ms": tf_all,
+                        "tau_c_ms": tc_all, "tau_c_over_tau_f": r, "N_c_over_N_f": nc / nf,
+                        "defects": dlist},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "rk4_stage S1..S4 (stencil_kernel<1..4>): one RK4 step = 4 launches",
+                         "algorithmic_bytes_per_launch": FINE_BYTES_PER_PT * n ** 3,
+                         "launch_ms": t_fine_step_ms, "peak_source": peak_src,
+                         "point_steps_per_s": n ** 3 / (t_fine_step_ms / 1e3)},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    grid.destroy()
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,411 @@
+// kernels.cuh — sm_100a kernels of the hot path.
+//
+//   stencil_kernel<K_COARSE>  one forward-Euler step of G  (Alg.2)
+//   stencil_kernel<K_S1..S4>  the four fused stages of one classical RK4 step
+//                             of F, RHS fused with the stage axpys
+//   correct_kernel            Parareal correction u = f + (g_new - g_old)
+//                             (Alg.1 line alg_para_corr) with the fused
+//                             max-norm of Eq.(defect)
+//   maxabs_kernel             max|u - ref| and max|ref|  (Eq.(defect))
+//   fill_sine_kernel          u0 = sin sin sin
+//
+// Field layout: n^3 fp64, index (z*n + y)*n + x.  Periodic wrap is done while
+// loading tiles (no ghost cells in memory).
+//
+// Stencil kernels: a CTA owns an (x,y) tile of TX x TY points and marches a
+// chunk of z planes.  Each plane of the stencil input (with a 2-point x halo
+// and an R-point y halo, wrapped periodically) and each plane of the
+// pointwise inputs is fetched by the TMA bulk-copy engine
+// (cp.async.bulk ... mbarrier::complete_tx) into a DEPTH-slot shared-memory
+// ring, several planes ahead of the compute.  z neighbours live in a per-thread
+// register queue; x/y neighbours are read from the current shared-memory
+// plane.  Outputs are written straight to global memory, coalesced along x.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace prk {
+
+enum Kind { K_COARSE = 0, K_S1 = 1, K_S2 = 2, K_S3 = 3, K_S4 = 4 };
+
+constexpr int TX = 32;            // tile width (one warp along x)
+constexpr int TY = 16;            // tile height
+constexpr int RPT = 4;            // consecutive y rows per thread
+constexpr int BY = TY / RPT;      // thread rows per CTA
+constexpr int NTHREADS = TX * BY; // 128
+constexpr int HX = 2;             // x halo kept in smem (2 => 16-byte aligned rows)
+constexpr int SX = TX + 2 * HX;   // smem row stride in doubles (36)
+constexpr int DEPTH = 6;          // ring slots (planes in flight + in use)
+
+template <int KIND> struct Traits;
+template <> struct Traits<K_COARSE> { static constexpr int R = 1, NP = 0; };
+template <> struct Traits<K_S1> { static constexpr int R = 2, NP = 0; };  // reads u*
+template <> struct Traits<K_S2> { static constexpr int R = 2, NP = 2; };  // Ya*, u, acc
+template <> struct Traits<K_S3> { static constexpr int R = 2, NP = 2; };  // Yb*, u, acc
+template <> struct Traits<K_S4> { static constexpr int R = 2, NP = 1; };  // Ya*, acc
+
+template <int KIND> struct Layout {
+    static constexpr int R = Traits<KIND>::R, NP = Traits<KIND>::NP;
+    static constexpr int Y_ELEMS = (TY + 2 * R) * SX;   // stencil plane with halos
+    static constexpr int P_ELEMS = TY * TX;             // one pointwise plane
+    static constexpr int SLOT_ELEMS = Y_ELEMS + NP * P_ELEMS;
+    static constexpr size_t SMEM_BYTES = size_t(DEPTH) * SLOT_ELEMS * sizeof(double);
+};
+
+struct StencilArgs {
+    const double *y;    // stencil input (read with halo)
+    const double *p0;   // pointwise input 0 (u for S2/S3, acc for S4)
+    const double *p1;   // pointwise input 1 (acc for S2/S3)
+    double *o0;         // output 0 (acc for S1-S3, u for S4, u' for coarse)
+    double *o1;         // output 1 (Ya for S1/S3, Yb for S2)
+    const double *nu_tab;      // nu per (step, stage): fine 4/step, coarse 1/step
+    const long long *nu_pos;   // device cursor: table row of local step 0
+    int j_local;               // step index inside the launch batch
+    int n;
+    int tiles_x, tiles_y, cz, chunks_z;
+    double inv_dx;      // 1/dx
+    double c[3];        // advection velocity
+    double dt;          // step size (delta t or Delta t)
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ int wrapi(int i, int n) {
+    i %= n;
+    return i < 0 ? i + n : i;
+}
+
+// Issue the bulk copies of stream element e (plane z_begin - R + e) into its
+// ring slot.  Executed by all 32 lanes of warp 0.
+template <int KIND>
+__device__ __forceinline__ void issue_element(const StencilArgs &a, double *ring, uint64_t *bars,
+                                              int e, int z_begin, int nz, int x0, int w, int y0,
+                                              int h, int lane) {
+    using L = Layout<KIND>;
+    constexpr int R = L::R, NP = L::NP;
+    const int n = a.n;
+    const int slot = e % DEPTH;
+    double *ys = ring + size_t(slot) * L::SLOT_ELEMS;
+    const int z = wrapi(z_begin - R + e, n);
+    const bool pw = NP > 0 && e >= R && e < nz + R;
+    const int yrows = h + 2 * R;
+    const uint32_t bytes = uint32_t(yrows) * uint32_t(w + 2 * HX) * 8u +
+                           (pw ? uint32_t(NP) * uint32_t(h) * uint32_t(w) * 8u : 0u);
+    if (lane == 0) mbar_arrive_expect_tx(&bars[slot], bytes);
+    __syncwarp();
+    const size_t plane = size_t(z) * n * n;
+    for (int r = lane; r < yrows; r += 32) {
+        const int yy = wrapi(y0 - R + r, n);
+        const double *row = a.y + plane + size_t(yy) * n;
+        double *dst = ys + r * SX;
+        int s = x0 - HX, left = w + 2 * HX, off = 0;
+        while (left > 0) {  // periodic pieces of [x0-2, x0+w+2)
+            const int src = wrapi(s, n);
+            const int m = min(left, n - src);
+            bulk_g2s(dst + off, row + src, uint32_t(m) * 8u, &bars[slot]);
+            s += m; off += m; left -= m;
+        }
+    }
+    if (pw) {
+        const int zz = z;  // pointwise planes are never wrapped (R <= e < nz+R)
+        for (int q = lane; q < NP * h; q += 32) {
+            const int f = q / h, r = q % h;
+            const double *src = (f == 0 ? a.p0 : a.p1) + size_t(zz) * n * n + size_t(y0 + r) * n + x0;
+            double *dst = ys + L::Y_ELEMS + f * L::P_ELEMS + r * TX;
+            bulk_g2s(dst, src, uint32_t(w) * 8u, &bars[slot]);
+        }
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(NTHREADS)
+stencil_kernel(const StencilArgs a) {
+    using L = Layout<KIND>;
+    constexpr int R = L::R, NP = L::NP, Q = 2 * R + 1;
+    extern __shared__ __align__(128) double ring[];
+    __shared__ __align__(8) uint64_t bars[DEPTH];
+
+    const int n = a.n;
+    int b = blockIdx.x;
+    const int tix = b % a.tiles_x; b /= a.tiles_x;
+    const int tiy = b % a.tiles_y; b /= a.tiles_y;
+    const int cz = b;
+    const int x0 = tix * TX, y0 = tiy * TY;
+    const int w = min(TX, n - x0), h = min(TY, n - y0);
+    const int z_begin = cz * a.cz;
+    const int nz = min(a.cz, n - z_begin);
+    const int E = nz + 2 * R;
+
+    const int tx = threadIdx.x % TX;
+    const int ty = threadIdx.x / TX;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int row0 = ty * RPT;  // first tile row of this thread
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < DEPTH; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    int e_next = 0;
+    if (warp == 0) {
+        for (; e_next < DEPTH && e_next < E; ++e_next)
+            issue_element<KIND>(a, ring, bars, e_next, z_begin, nz, x0, w, y0, h, lane);
+    } else {
+        e_next = min(DEPTH, E);
+    }
+
+    // Coefficients (read after the prologue copies are in flight).
+    const double nu = a.nu_tab[(*a.nu_pos + a.j_local) * (KIND == K_COARSE ? 1 : 4) +
+                               (KIND == K_COARSE ? 0 : KIND - 1)];
+    // Per-neighbour weights of the folded operator: L = w0 y + sum_a sum_o w_{a,o} y_{+o e_a}
+    double wm2[3], wm1[3], wp1[3], wp2[3], w0;
+    if (KIND == K_COARSE) {
+        // rhs = nu (sum6 - 6u)/dx^2 - sum_a c_a upwind_a(u)/dx   (Alg.2)
+        const double al = nu * a.inv_dx * a.inv_dx;
+        w0 = -6.0 * al;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double b1 = a.c[d] * a.inv_dx;
+            if (a.c[d] > 0) {  // backward difference: -c (u - u_-)/dx
+                wm1[d] = al + b1; wp1[d] = al; w0 -= b1;
+            } else {           // forward difference: -c (u_+ - u)/dx
+                wm1[d] = al; wp1[d] = al - b1; w0 += b1;
+            }
+            wm2[d] = wp2[d] = 0.0;
+        }
+    } else {
+        // rhs = nu Lap4 u - c . Grad4 u  with weights (-1,16,-30,16,-1)/12dx^2
+        // and (-1,8,0,-8,1)/12dx on offsets (+2,+1,0,-1,-2)   (C3)
+        const double al = nu * a.inv_dx * a.inv_dx / 12.0;
+        w0 = -90.0 * al;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double be = a.c[d] * a.inv_dx / 12.0;
+            wp2[d] = -al + be; wp1[d] = 16.0 * al - 8.0 * be;
+            wm1[d] = 16.0 * al + 8.0 * be; wm2[d] = -al - be;
+        }
+    }
+    const double dt = a.dt;
+
+    const bool col_ok = tx < w;
+    double q[RPT][Q];  // z queue: q[r][R + o] = Y(z + o) at (x, row0 + r)
+
+    for (int i = 0; i < nz; ++i) {
+        if (i == 0) {
+            for (int e = 0; e < 2 * R; ++e) {
+                mbar_wait(&bars[e % DEPTH], (e / DEPTH) & 1);
+                const double *ys = ring + size_t(e % DEPTH) * L::SLOT_ELEMS;
+#pragma unroll
+                for (int r = 0; r < RPT; ++r)
+                    q[r][e] = ys[(R + row0 + r) * SX + HX + tx];
+            }
+        }
+        {
+            const int e = i + 2 * R;
+            mbar_wait(&bars[e % DEPTH], (e / DEPTH) & 1);
+            const double *ys = ring + size_t(e % DEPTH) * L::SLOT_ELEMS;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) q[r][2 * R] = ys[(R + row0 + r) * SX + HX + tx];
+        }
+        const int ec = i + R;  // element holding the centre plane
+        const double *ys = ring + size_t(ec % DEPTH) * L::SLOT_ELEMS;
+        const double *ps = ys + L::Y_ELEMS;
+        const int z = z_begin + i;
+
+        // y column above/below the RPT rows (centres come from the queue)
+        double col[RPT + 2 * R];
+#pragma unroll
+        for (int r = 0; r < RPT + 2 * R; ++r) {
+            if (r >= R && r < R + RPT) continue;
+            col[r] = ys[(row0 + r) * SX + HX + tx];
+        }
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            col[R + r] = q[r][R];
+        }
+
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const int row = row0 + r;
+            const double *yrow = ys + (R + row) * SX + HX + tx;
+            const double yc = q[r][R];
+            double acc = w0 * yc;
+            // x neighbours
+            if constexpr (R == 2) acc = fma(wm2[0], yrow[-2], acc);
+            acc = fma(wm1[0], yrow[-1], acc);
+            acc = fma(wp1[0], yrow[1], acc);
+            if constexpr (R == 2) acc = fma(wp2[0], yrow[2], acc);
+            // y neighbours (col index R + r is the centre)
+            if constexpr (R == 2) acc = fma(wm2[1], col[r + R - 2], acc);
+            acc = fma(wm1[1], col[r + R - 1], acc);
+            acc = fma(wp1[1], col[r + R + 1], acc);
+            if constexpr (R == 2) acc = fma(wp2[1], col[r + R + 2], acc);
+            // z neighbours from the queue
+            if constexpr (R == 2) acc = fma(wm2[2], q[r][R - 2], acc);
+            acc = fma(wm1[2], q[r][R - 1], acc);
+            acc = fma(wp1[2], q[r][R + 1], acc);
+            if constexpr (R == 2) acc = fma(wp2[2], q[r][R + 2], acc);
+            const double Lv = acc;  // the right-hand side at this point
+
+            if (col_ok && row < h) {
+                const size_t g = (size_t(z) * n + (y0 + row)) * n + x0 + tx;
+                if (KIND == K_COARSE) {
+                    a.o0[g] = yc + dt * Lv;
+                } else if (KIND == K_S1) {                        // y = u
+                    a.o0[g] = yc + (dt / 6.0) * Lv;               // acc = u + dt/6 k1
+                    a.o1[g] = yc + (dt / 2.0) * Lv;               // Ya  = u + dt/2 k1
+                } else if (KIND == K_S2) {
+                    const double u = ps[row * TX + tx], ac = ps[L::P_ELEMS + row * TX + tx];
+                    a.o0[g] = ac + (dt / 3.0) * Lv;               // acc += dt/3 k2
+                    a.o1[g] = u + (dt / 2.0) * Lv;                // Yb  = u + dt/2 k2
+                } else if (KIND == K_S3) {
+                    const double u = ps[row * TX + tx], ac = ps[L::P_ELEMS + row * TX + tx];
+                    a.o0[g] = ac + (dt / 3.0) * Lv;               // acc += dt/3 k3
+                    a.o1[g] = u + dt * Lv;                        // Ya  = u + dt k3
+                } else {                                          // K_S4
+                    const double ac = ps[row * TX + tx];
+                    a.o0[g] = ac + (dt / 6.0) * Lv;               // u = acc + dt/6 k4
+                }
+            }
+        }
+        (void)NP;
+        // shift the z queue
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+#pragma unroll
+            for (int o = 0; o < Q - 1; ++o) q[r][o] = q[r][o + 1];
+
+        __syncthreads();  // every read of element i + R (and earlier) is done
+        if (warp == 0) {
+            bool fenced = false;
+            while (e_next < E && e_next - DEPTH <= i + R) {
+                if (!fenced) { fence_proxy_async(); fenced = true; }
+                issue_element<KIND>(a, ring, bars, e_next, z_begin, nz, x0, w, y0, h, lane);
+                ++e_next;
+            }
+        } else {
+            while (e_next < E && e_next - DEPTH <= i + R) ++e_next;
+        }
+    }
+}
+
+// Advance the nu-table cursor after a batch of steps (last node of a graph).
+__global__ void advance_pos_kernel(long long *pos, long long by) { *pos += by; }
+__global__ void set_pos_kernel(long long *pos, long long v) { *pos = v; }
+
+// ------------------------------------------------------------ reductions
+// max of non-negative doubles via their IEEE bit patterns (monotone for >= 0;
+// a positive NaN compares above +inf, so NaN propagates).
+__device__ __forceinline__ unsigned long long abs_bits(double v) {
+    return static_cast<unsigned long long>(__double_as_longlong(fabs(v)));
+}
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+    return a > b ? a : b;
+}
+__device__ __forceinline__ unsigned long long warp_max(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = umax64(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+template <int NT>
+__device__ __forceinline__ void block_max_atomic(unsigned long long v, unsigned long long *dst) {
+    __shared__ unsigned long long sred[NT / 32];
+    v = warp_max(v);
+    if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        unsigned long long t = threadIdx.x < NT / 32 ? sred[threadIdx.x] : 0ull;
+        t = warp_max(t);
+        if (threadIdx.x == 0 && t) atomicMax(dst, t);
+    }
+}
+
+constexpr int RED_THREADS = 256;
+
+// u_out = f + (g_new - g_old)  [C5];  optional max|u_out - u_ref| -> *dmax
+__global__ void __launch_bounds__(RED_THREADS)
+correct_kernel(const double2 *__restrict__ f, const double2 *__restrict__ gn,
+               const double2 *__restrict__ go, double2 *uo, const double2 *__restrict__ ref,
+               unsigned long long *dmax, long long n2) {
+    unsigned long long m = 0;
+    for (long long i = blockIdx.x * (long long)RED_THREADS + threadIdx.x; i < n2;
+         i += (long long)gridDim.x * RED_THREADS) {
+        const double2 a = f[i], b = gn[i], c = go[i];
+        double2 v;
+        v.x = a.x + (b.x - c.x);
+        v.y = a.y + (b.y - c.y);
+        uo[i] = v;
+        if (ref) {
+            const double2 r = __ldcs(ref + i);
+            m = umax64(m, umax64(abs_bits(v.x - r.x), abs_bits(v.y - r.y)));
+        }
+    }
+    if (ref) block_max_atomic<RED_THREADS>(m, dmax);
+}
+
+// *d_diff = max|u - ref| (if u and d_diff), *d_ref = max|ref| (if d_ref)
+__global__ void __launch_bounds__(RED_THREADS)
+maxabs_kernel(const double2 *__restrict__ u, const double2 *__restrict__ ref,
+              unsigned long long *d_diff, unsigned long long *d_ref, long long n2) {
+    unsigned long long m0 = 0, m1 = 0;
+    for (long long i = blockIdx.x * (long long)RED_THREADS + threadIdx.x; i < n2;
+         i += (long long)gridDim.x * RED_THREADS) {
+        const double2 r = ref[i];
+        m1 = umax64(m1, umax64(abs_bits(r.x), abs_bits(r.y)));
+        if (u) {
+            const double2 v = u[i];
+            m0 = umax64(m0, umax64(abs_bits(v.x - r.x), abs_bits(v.y - r.y)));
+        }
+    }
+    if (d_ref) block_max_atomic<RED_THREADS>(m1, d_ref);
+    __syncthreads();
+    if (u && d_diff) block_max_atomic<RED_THREADS>(m0, d_diff);
+}
+
+// u[z][y][x] = (s[x] s[y]) s[z], s[i] = sin(2 pi i dx) from the host
+__global__ void fill_sine_kernel(const double *__restrict__ s, double *u, int n) {
+    const long long N = (long long)n * n * n;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int x = int(i % n), y = int((i / n) % n), z = int(i / ((long long)n * n));
+        u[i] = s[x] * s[y] * s[z];
+    }
+}
+
+}  // namespace prk

@@ -1,0 +1,1036 @@
+// parareal.cu — C ABI (include/parareal.h) and host runtime of the B200 hot
+// path: nu tables, CUDA-graph batches of stencil steps, the Parareal driver
+// (Alg.1) and its NCCL point-to-point pipeline.
+//
+// Nothing here includes or calls the CPU oracle (oracle/); this file and
+// kernels.cuh are the whole product path.
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <thread>
+#include <utility>
+#include <vector>
+
+#include "../../include/parareal.h"
+#include "kernels.cuh"
+
+using namespace prk;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+static pr_status fail(pr_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(e_ == cudaErrorMemoryAllocation ? PR_ENOMEM : PR_ECUDA,            \
+                        "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                        \
+    } while (0)
+#define CKS(expr)                          \
+    do {                                   \
+        pr_status s_ = (expr);             \
+        if (s_ != PR_OK) return s_;        \
+    } while (0)
+#define CKL()                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = cudaGetLastError();                                               \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(PR_ECUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                               \
+    } while (0)
+
+// ------------------------------------------------------------------ grid
+namespace {
+
+struct LaunchCfg {
+    int tiles_x = 0, tiles_y = 0, cz = 0, chunks_z = 0, blocks = 0, occ = 0;
+};
+
+struct NuTable {
+    double *d = nullptr;
+    size_t cap = 0;          // doubles
+    int64_t lo = 0, hi = 0;  // global step range covered
+    double dt = 0.0;
+    bool valid = false;
+};
+
+constexpr int FINE_BATCH = 16;    // RK4 steps per CUDA graph (64 kernels)
+constexpr int COARSE_PAIRS = 16;  // Euler step pairs per CUDA graph (32 kernels)
+
+}  // namespace
+
+struct pr_grid {
+    int dev = 0;
+    pr_problem prob{};
+    int n = 0;
+    int64_t N = 0;
+    size_t bytes = 0;
+    int sms = 0;
+    cudaStream_t cap_stream = nullptr;  // private stream used only for graph capture
+    double *acc = nullptr, *ya = nullptr, *yb = nullptr, *ctmp = nullptr;
+    double *d_sine = nullptr;
+    long long *d_pos = nullptr;             // [0] fine cursor, [1] coarse cursor
+    unsigned long long *d_red = nullptr;    // reduction slots
+    unsigned long long *h_red = nullptr;    // pinned mirror
+    int red_cap = 0;
+    NuTable tab_f, tab_c;
+    double *h_stage = nullptr;              // pinned staging for nu tables
+    size_t h_stage_cap = 0;
+    cudaEvent_t stage_ev = nullptr;         // last table upload
+    LaunchCfg lc[5];
+    std::map<std::pair<int, const void *>, std::pair<cudaGraphExec_t, int>> graphs;
+    // host-pointer staging
+    double *stage_a = nullptr, *stage_b = nullptr;
+    // Parareal state
+    int par_s = 0;
+    std::vector<double *> pool;
+    // NCCL
+    ncclComm_t comm = nullptr;
+    int world = 1, rank = 0;
+    cudaStream_t comm_stream = nullptr;
+    std::vector<cudaEvent_t> evs, dep_evs;
+    double timings[5] = {0, 0, 0, 0, 0};
+};
+
+template <int KIND>
+static pr_status setup_kind(pr_grid *g) {
+    const size_t smem = Layout<KIND>::SMEM_BYTES;
+    CK(cudaFuncSetAttribute(stencil_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(smem)));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil_kernel<KIND>, NTHREADS, smem));
+    if (occ < 1) return fail(PR_ECUDA, "stencil kernel %d cannot be resident", KIND);
+    LaunchCfg &c = g->lc[KIND];
+    const int n = g->n;
+    c.occ = occ;
+    c.tiles_x = (n + TX - 1) / TX;
+    c.tiles_y = (n + TY - 1) / TY;
+    const int tiles = c.tiles_x * c.tiles_y;
+    const int slots = g->sms * occ;
+    const int R = Traits<KIND>::R;
+    // z-chunking: fill whole waves of resident CTAs while keeping the z halo
+    // re-read (2R planes per chunk) small.
+    int best_chunks = 1;
+    double best = -1.0;
+    const int min_cz = std::min(n, 8);
+    for (int ch = 1; ch <= n / min_cz; ++ch) {
+        const int cz = (n + ch - 1) / ch;
+        const int che = (n + cz - 1) / cz;
+        const long items = long(tiles) * che;
+        const long waves = (items + slots - 1) / slots;
+        const double eff = double(items) / double(waves * slots);
+        const double over = 1.0 + 0.5 * double(2 * R) / double(cz);
+        const double score = eff / over;
+        if (score > best + 1e-9) { best = score; best_chunks = che; }
+    }
+    if (const char *env = getenv("PR_CHUNKS_Z")) {
+        int v = atoi(env);
+        if (v >= 1 && v <= n) best_chunks = v;
+    }
+    c.cz = (n + best_chunks - 1) / best_chunks;
+    c.chunks_z = (n + c.cz - 1) / c.cz;
+    c.blocks = tiles * c.chunks_z;
+    return PR_OK;
+}
+
+static StencilArgs base_args(const pr_grid *g, int kind) {
+    StencilArgs a{};
+    const LaunchCfg &c = g->lc[kind];
+    a.n = g->n;
+    a.tiles_x = c.tiles_x;
+    a.tiles_y = c.tiles_y;
+    a.cz = c.cz;
+    a.chunks_z = c.chunks_z;
+    a.inv_dx = double(g->n);  // dx = 1/n
+    for (int d = 0; d < 3; ++d) a.c[d] = g->prob.c[d];
+    return a;
+}
+
+template <int KIND>
+static void launch_stencil(pr_grid *g, const StencilArgs &a0, cudaStream_t st) {
+    StencilArgs a = a0;  // tile decomposition of this kind (occupancy differs per kind)
+    const LaunchCfg &c = g->lc[KIND];
+    a.tiles_x = c.tiles_x;
+    a.tiles_y = c.tiles_y;
+    a.cz = c.cz;
+    a.chunks_z = c.chunks_z;
+    stencil_kernel<KIND><<<c.blocks, NTHREADS, Layout<KIND>::SMEM_BYTES, st>>>(a);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+// One classical RK4 step as four fused stage passes.
+static void enqueue_fine_step(pr_grid *g, const double *u_src, double *u_dst, int j_local,
+                              double dt, cudaStream_t st) {
+    StencilArgs a = base_args(g, K_S1);
+    a.nu_tab = g->tab_f.d;
+    a.nu_pos = g->d_pos + 0;
+    a.j_local = j_local;
+    a.dt = dt;
+    // S1: k1 = L(u); acc = u + dt/6 k1; Ya = u + dt/2 k1
+    a.y = u_src; a.p0 = nullptr; a.p1 = nullptr; a.o0 = g->acc; a.o1 = g->ya;
+    launch_stencil<K_S1>(g, a, st);
+    // S2: k2 = L(Ya); acc += dt/3 k2; Yb = u + dt/2 k2
+    a.y = g->ya; a.p0 = u_src; a.p1 = g->acc; a.o0 = g->acc; a.o1 = g->yb;
+    launch_stencil<K_S2>(g, a, st);
+    // S3: k3 = L(Yb); acc += dt/3 k3; Ya = u + dt k3
+    a.y = g->yb; a.p0 = u_src; a.p1 = g->acc; a.o0 = g->acc; a.o1 = g->ya;
+    launch_stencil<K_S3>(g, a, st);
+    // S4: k4 = L(Ya); u = acc + dt/6 k4
+    a.y = g->ya; a.p0 = g->acc; a.p1 = nullptr; a.o0 = u_dst; a.o1 = nullptr;
+    launch_stencil<K_S4>(g, a, st);
+}
+
+// One forward-Euler step (Alg.2).
+static void enqueue_coarse_step(pr_grid *g, const double *src, double *dst, int j_local,
+                                double dt, cudaStream_t st) {
+    StencilArgs a = base_args(g, K_COARSE);
+    a.nu_tab = g->tab_c.d;
+    a.nu_pos = g->d_pos + 1;
+    a.j_local = j_local;
+    a.dt = dt;
+    a.y = src;
+    a.o0 = dst;
+    launch_stencil<K_COARSE>(g, a, st);
+}
+
+static pr_status set_pos(pr_grid *g, int which, long long v, cudaStream_t st) {
+    set_pos_kernel<<<1, 1, 0, st>>>(g->d_pos + which, v);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    CKL();
+    return PR_OK;
+}
+
+// nu(t) = nu0 + nu0/2 sin(omega t)
+static inline double nu_of(const pr_problem &p, double t) {
+    return p.nu0 + (p.nu0 / 2.0) * std::sin(p.omega * t);
+}
+
+static void clear_graphs(pr_grid *g, int kind) {
+    for (auto it = g->graphs.begin(); it != g->graphs.end();) {
+        if (it->first.first == kind) {
+            cudaGraphExecDestroy(it->second.first);
+            it = g->graphs.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+
+// Make the device nu table of `fine` (0/1) cover global steps [lo, hi) of size dt.
+static pr_status ensure_table(pr_grid *g, int fine, double dt, int64_t lo, int64_t hi,
+                              cudaStream_t st) {
+    NuTable &T = fine ? g->tab_f : g->tab_c;
+    if (T.valid && T.dt == dt && lo >= T.lo && hi <= T.hi) return PR_OK;
+    const int per = fine ? 4 : 1;
+    const size_t need = size_t(std::max<int64_t>(hi - lo, 1)) * per;
+    if (need > T.cap) {
+        CK(cudaStreamSynchronize(st));
+        if (T.d) CK(cudaFree(T.d));
+        T.d = nullptr;
+        const size_t cap = std::max(need, T.cap * 2);
+        CK(cudaMalloc(&T.d, cap * sizeof(double)));
+        T.cap = cap;
+        clear_graphs(g, fine ? 0 : 1);  // graphs captured the old table pointer
+    }
+    if (need > g->h_stage_cap) {
+        CK(cudaEventSynchronize(g->stage_ev));
+        if (g->h_stage) CK(cudaFreeHost(g->h_stage));
+        g->h_stage = nullptr;
+        CK(cudaMallocHost(&g->h_stage, need * sizeof(double)));
+        g->h_stage_cap = need;
+    }
+    CK(cudaEventSynchronize(g->stage_ev));  // previous upload has consumed the staging buffer
+    const pr_problem &p = g->prob;
+    for (int64_t j = lo; j < hi; ++j) {
+        double *r = g->h_stage + size_t(j - lo) * per;
+        if (!fine) {
+            r[0] = nu_of(p, double(j) * dt);  // nu at the step start (C2)
+        } else if (p.nu_mode == PR_NU_STEP_START) {
+            r[0] = r[1] = r[2] = r[3] = nu_of(p, double(j) * dt);
+        } else {  // stage times t_j, t_j + dt/2, t_j + dt/2, t_j + dt (C1, C6)
+            r[0] = nu_of(p, double(j) * dt);
+            r[1] = r[2] = nu_of(p, (double(j) + 0.5) * dt);
+            r[3] = nu_of(p, (double(j) + 1.0) * dt);
+        }
+    }
+    CK(cudaMemcpyAsync(T.d, g->h_stage, size_t(hi - lo) * per * sizeof(double),
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(g->stage_ev, st));
+    T.lo = lo;
+    T.hi = hi;
+    T.dt = dt;
+    T.valid = true;
+    return PR_OK;
+}
+
+// Cached CUDA graph: FINE_BATCH RK4 steps in place on `u` (kind 0), or
+// COARSE_PAIRS Euler step pairs u -> tmp -> u (kind 1); the last node
+// advances the nu cursor.  The step size is baked in, so the key includes it
+// through the table (re-captured when the table pointer changes).
+static pr_status get_graph(pr_grid *g, int kind, double *u, double dt, cudaGraphExec_t *out) {
+    auto key = std::make_pair(kind, (const void *)u);
+    auto it = g->graphs.find(key);
+    if (it != g->graphs.end() && it->second.second == int(std::hash<double>{}(dt) & 0x7fffffff)) {
+        *out = it->second.first;
+        return PR_OK;
+    }
+    if (it != g->graphs.end()) {
+        cudaGraphExecDestroy(it->second.first);
+        g->graphs.erase(it);
+    }
+    cudaGraph_t graph;
+    const long long before = g_launches.load();
+    CK(cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal));
+    if (kind == 0) {
+        for (int b = 0; b < FINE_BATCH; ++b) enqueue_fine_step(g, u, u, b, dt, g->cap_stream);
+        advance_pos_kernel<<<1, 1, 0, g->cap_stream>>>(g->d_pos + 0, FINE_BATCH);
+    } else {
+        for (int b = 0; b < COARSE_PAIRS; ++b) {
+            enqueue_coarse_step(g, u, g->ctmp, 2 * b, dt, g->cap_stream);
+            enqueue_coarse_step(g, g->ctmp, u, 2 * b + 1, dt, g->cap_stream);
+        }
+        advance_pos_kernel<<<1, 1, 0, g->cap_stream>>>(g->d_pos + 1, 2 * COARSE_PAIRS);
+    }
+    cudaError_t ce = cudaStreamEndCapture(g->cap_stream, &graph);
+    g_launches.store(before);  // capture does not launch
+    if (ce != cudaSuccess)
+        return fail(PR_ECUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+    cudaGraphExec_t exec;
+    ce = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess)
+        return fail(PR_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
+    if (g->graphs.size() > 64) {  // bound the cache
+        clear_graphs(g, 0);
+        clear_graphs(g, 1);
+    }
+    g->graphs[key] = std::make_pair(exec, int(std::hash<double>{}(dt) & 0x7fffffff));
+    *out = exec;
+    return PR_OK;
+}
+
+static pr_status run_fine(pr_grid *g, const double *uin, double *uout, int64_t step0,
+                          int64_t nsteps, double dt, cudaStream_t st) {
+    if (nsteps == 0) {
+        if (uin != uout) CK(cudaMemcpyAsync(uout, uin, g->bytes, cudaMemcpyDeviceToDevice, st));
+        return PR_OK;
+    }
+    CKS(ensure_table(g, 1, dt, step0, step0 + nsteps, st));
+    const long long base = step0 - g->tab_f.lo;
+    int64_t done = 0;
+    CKS(set_pos(g, 0, base, st));
+    if (uin != uout) {  // first step reads u_in, writes u_out; later steps in place
+        enqueue_fine_step(g, uin, uout, 0, dt, st);
+        CKL();
+        done = 1;
+        CKS(set_pos(g, 0, base + 1, st));
+    }
+    if (nsteps - done >= FINE_BATCH) {
+        cudaGraphExec_t ge;
+        CKS(get_graph(g, 0, uout, dt, &ge));
+        while (nsteps - done >= FINE_BATCH) {
+            CK(cudaGraphLaunch(ge, st));
+            g_launches.fetch_add(4 * FINE_BATCH + 1, std::memory_order_relaxed);
+            done += FINE_BATCH;
+        }
+    }
+    for (int b = 0; done < nsteps; ++b, ++done) enqueue_fine_step(g, uout, uout, b, dt, st);
+    CKL();
+    return PR_OK;
+}
+
+static pr_status run_coarse(pr_grid *g, const double *uin, double *uout, int64_t step0,
+                            int64_t nsteps, double dt, cudaStream_t st) {
+    if (nsteps == 0) {
+        if (uin != uout) CK(cudaMemcpyAsync(uout, uin, g->bytes, cudaMemcpyDeviceToDevice, st));
+        return PR_OK;
+    }
+    CKS(ensure_table(g, 0, dt, step0, step0 + nsteps, st));
+    const long long base = step0 - g->tab_c.lo;
+    int64_t done = 0;
+    CKS(set_pos(g, 1, base, st));
+    int jl = 0;
+    if (uin != uout) {
+        if (nsteps % 2) {  // odd: u_in -> u_out, then pairs on u_out
+            enqueue_coarse_step(g, uin, uout, jl++, dt, st);
+            done = 1;
+        } else {           // even: u_in -> tmp -> u_out, then pairs on u_out
+            enqueue_coarse_step(g, uin, g->ctmp, jl++, dt, st);
+            enqueue_coarse_step(g, g->ctmp, uout, jl++, dt, st);
+            done = 2;
+        }
+        CKL();
+        CKS(set_pos(g, 1, base + done, st));
+        jl = 0;
+    }
+    const int64_t pairs = (nsteps - done) / 2;
+    int64_t p = 0;
+    if (pairs >= COARSE_PAIRS) {
+        cudaGraphExec_t ge;
+        CKS(get_graph(g, 1, uout, dt, &ge));
+        for (; p + COARSE_PAIRS <= pairs; p += COARSE_PAIRS) {
+            CK(cudaGraphLaunch(ge, st));
+            g_launches.fetch_add(2 * COARSE_PAIRS + 1, std::memory_order_relaxed);
+            done += 2 * COARSE_PAIRS;
+        }
+    }
+    for (; p < pairs; ++p) {
+        enqueue_coarse_step(g, uout, g->ctmp, jl++, dt, st);
+        enqueue_coarse_step(g, g->ctmp, uout, jl++, dt, st);
+        done += 2;
+    }
+    if (done < nsteps) {  // in place with an odd count: last step via tmp + copy
+        enqueue_coarse_step(g, uout, g->ctmp, jl++, dt, st);
+        CK(cudaMemcpyAsync(uout, g->ctmp, g->bytes, cudaMemcpyDeviceToDevice, st));
+        ++done;
+    }
+    CKL();
+    return PR_OK;
+}
+
+static int red_blocks(const pr_grid *g) { return g->sms * 4; }
+
+static pr_status ensure_red(pr_grid *g, int slots) {
+    if (slots <= g->red_cap) return PR_OK;
+    if (g->d_red) CK(cudaFree(g->d_red));
+    if (g->h_red) CK(cudaFreeHost(g->h_red));
+    g->d_red = nullptr;
+    g->h_red = nullptr;
+    CK(cudaMalloc(&g->d_red, slots * sizeof(unsigned long long)));
+    CK(cudaMallocHost(&g->h_red, slots * sizeof(unsigned long long)));
+    g->red_cap = slots;
+    return PR_OK;
+}
+
+static double bits_to_double(unsigned long long b) {
+    double d;
+    std::memcpy(&d, &b, sizeof d);
+    return d;
+}
+
+static bool is_host_ptr(const void *p) {
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+}
+
+static pr_status ensure_stage(pr_grid *g) {
+    if (!g->stage_a) CK(cudaMalloc(&g->stage_a, g->bytes));
+    if (!g->stage_b) CK(cudaMalloc(&g->stage_b, g->bytes));
+    return PR_OK;
+}
+
+static bool overlaps(const void *a, const void *b, size_t bytes) {
+    const char *x = static_cast<const char *>(a), *y = static_cast<const char *>(b);
+    return x < y + bytes && y < x + bytes;
+}
+
+static pr_status check_grid(pr_grid *g) {
+    if (!g) return fail(PR_EINVAL, "grid is NULL");
+    CK(cudaSetDevice(g->dev));
+    return PR_OK;
+}
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+const char *pr_last_error(void) { return g_err.c_str(); }
+const char *pr_version(void) { return "parareal-b200 0.1 (sm_100a)"; }
+int64_t pr_kernel_launches(void) { return g_launches.load(); }
+
+pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid **out) {
+    if (!problem || !out) return fail(PR_EINVAL, "null argument");
+    *out = nullptr;
+    const int n = problem->n;
+    if (n < 4 || n > 2048 || n % 2) return fail(PR_EINVAL, "n must be even and in [4, 2048], got %d", n);
+    if (!(problem->nu0 >= 0.0) || !(problem->T > 0.0) || !std::isfinite(problem->omega))
+        return fail(PR_EINVAL, "need nu0 >= 0, T > 0, finite omega");
+    for (int d = 0; d < 3; ++d)
+        if (!std::isfinite(problem->c[d])) return fail(PR_EINVAL, "non-finite velocity");
+    if (problem->nu_mode != PR_NU_STAGE && problem->nu_mode != PR_NU_STEP_START)
+        return fail(PR_EINVAL, "bad nu_mode %d", problem->nu_mode);
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (cuda_device < 0 || cuda_device >= ndev)
+        return fail(PR_EINVAL, "cuda_device %d out of range (%d devices)", cuda_device, ndev);
+    CK(cudaSetDevice(cuda_device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, cuda_device));
+    if (prop.major != 10)
+        return fail(PR_ECUDA, "this library is built for sm_100a (B200); device is sm_%d%d",
+                    prop.major, prop.minor);
+    pr_grid *g = new pr_grid();
+    g->dev = cuda_device;
+    g->prob = *problem;
+    g->n = n;
+    g->N = int64_t(n) * n * n;
+    g->bytes = size_t(g->N) * sizeof(double);
+    g->sms = prop.multiProcessorCount;
+    auto bail = [&](pr_status s) { pr_destroy_grid(g); return s; };
+#define GK(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return bail(fail(e_ == cudaErrorMemoryAllocation ? PR_ENOMEM : PR_ECUDA,         \
+                             "%s failed: %s", #call, cudaGetErrorString(e_)));              \
+    } while (0)
+    GK(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
+    GK(cudaEventCreateWithFlags(&g->stage_ev, cudaEventDisableTiming));
+    GK(cudaMalloc(&g->acc, g->bytes));
+    GK(cudaMalloc(&g->ya, g->bytes));
+    GK(cudaMalloc(&g->yb, g->bytes));
+    GK(cudaMalloc(&g->ctmp, g->bytes));
+    GK(cudaMalloc(&g->d_pos, 2 * sizeof(long long)));
+    GK(cudaMemset(g->d_pos, 0, 2 * sizeof(long long)));
+    GK(cudaMalloc(&g->d_sine, n * sizeof(double)));
+    {
+        std::vector<double> s(n);
+        const double dx = 1.0 / n;
+        for (int i = 0; i < n; ++i) s[i] = std::sin(2.0 * M_PI * (i * dx));
+        GK(cudaMemcpy(g->d_sine, s.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    pr_status s;
+    if ((s = setup_kind<K_COARSE>(g)) != PR_OK) return bail(s);
+    if ((s = setup_kind<K_S1>(g)) != PR_OK) return bail(s);
+    if ((s = setup_kind<K_S2>(g)) != PR_OK) return bail(s);
+    if ((s = setup_kind<K_S3>(g)) != PR_OK) return bail(s);
+    if ((s = setup_kind<K_S4>(g)) != PR_OK) return bail(s);
+    if ((s = ensure_red(g, 8)) != PR_OK) return bail(s);
+    // generous initial table capacities (graphs capture the pointers)
+    GK(cudaMalloc(&g->tab_f.d, (size_t(1) << 20) * sizeof(double)));
+    g->tab_f.cap = size_t(1) << 20;
+    GK(cudaMalloc(&g->tab_c.d, (size_t(1) << 18) * sizeof(double)));
+    g->tab_c.cap = size_t(1) << 18;
+#undef GK
+    *out = g;
+    return PR_OK;
+}
+
+pr_status pr_destroy_grid(pr_grid *g) {
+    if (!g) return PR_OK;
+    cudaSetDevice(g->dev);
+    cudaDeviceSynchronize();
+    for (auto &kv : g->graphs) cudaGraphExecDestroy(kv.second.first);
+    g->graphs.clear();
+    if (g->comm) ncclCommDestroy(g->comm);
+    for (double *p : g->pool) cudaFree(p);
+    cudaFree(g->acc); cudaFree(g->ya); cudaFree(g->yb); cudaFree(g->ctmp);
+    cudaFree(g->d_pos); cudaFree(g->d_red); cudaFree(g->d_sine);
+    cudaFree(g->tab_f.d); cudaFree(g->tab_c.d);
+    cudaFree(g->stage_a); cudaFree(g->stage_b);
+    if (g->h_red) cudaFreeHost(g->h_red);
+    if (g->h_stage) cudaFreeHost(g->h_stage);
+    for (cudaEvent_t e : g->evs) cudaEventDestroy(e);
+    for (cudaEvent_t e : g->dep_evs) cudaEventDestroy(e);
+    if (g->stage_ev) cudaEventDestroy(g->stage_ev);
+    if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
+    if (g->comm_stream) cudaStreamDestroy(g->comm_stream);
+    delete g;
+    return PR_OK;
+}
+
+static pr_status propagate(pr_grid *g, int fine, const double *u_in, double *u_out, int64_t step0,
+                           int64_t nsteps, double dt, void *stream) {
+    CKS(check_grid(g));
+    if (!u_in || !u_out) return fail(PR_EINVAL, "null field pointer");
+    if (nsteps < 0 || step0 < 0) return fail(PR_EINVAL, "need step0 >= 0 and n_steps >= 0");
+    if (!(dt > 0.0) || !std::isfinite(dt)) return fail(PR_EINVAL, "need dt > 0");
+    if (u_in != u_out && overlaps(u_in, u_out, g->bytes))
+        return fail(PR_EINVAL, "u_in and u_out overlap without being identical");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const bool hin = is_host_ptr(u_in), hout = is_host_ptr(u_out);
+    const double *din = u_in;
+    double *dout = u_out;
+    if (hin || hout) {
+        CKS(ensure_stage(g));
+        if (hin) {
+            CK(cudaMemcpyAsync(g->stage_a, u_in, g->bytes, cudaMemcpyHostToDevice, st));
+            din = g->stage_a;
+        }
+        if (hout) dout = (hin && u_in == u_out) ? g->stage_a : g->stage_b;
+    }
+    CKS(fine ? run_fine(g, din, dout, step0, nsteps, dt, st)
+             : run_coarse(g, din, dout, step0, nsteps, dt, st));
+    if (hout) {
+        CK(cudaMemcpyAsync(u_out, dout, g->bytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    } else if (hin) {
+        CK(cudaStreamSynchronize(st));
+    }
+    return PR_OK;
+}
+
+pr_status pr_fine(pr_grid *g, const double *u_in, double *u_out, int64_t step0, int64_t n_steps,
+                  double dt, void *stream) {
+    return propagate(g, 1, u_in, u_out, step0, n_steps, dt, stream);
+}
+
+pr_status pr_coarse(pr_grid *g, const double *u_in, double *u_out, int64_t step0,
+                    int64_t n_steps, double dt, void *stream) {
+    return propagate(g, 0, u_in, u_out, step0, n_steps, dt, stream);
+}
+
+static pr_status launch_maxabs(pr_grid *g, const double *u, const double *ref,
+                               unsigned long long *d_diff, unsigned long long *d_ref,
+                               cudaStream_t st) {
+    maxabs_kernel<<<red_blocks(g), RED_THREADS, 0, st>>>(
+        reinterpret_cast<const double2 *>(u), reinterpret_cast<const double2 *>(ref), d_diff,
+        d_ref, g->N / 2);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    CKL();
+    return PR_OK;
+}
+
+pr_status pr_defect(pr_grid *g, const double *u, const double *u_ref, double *d_host,
+                    void *stream) {
+    CKS(check_grid(g));
+    if (!u || !u_ref || !d_host) return fail(PR_EINVAL, "null argument");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const double *du = u, *dr = u_ref;
+    if (is_host_ptr(u) || is_host_ptr(u_ref)) {
+        CKS(ensure_stage(g));
+        if (is_host_ptr(u)) {
+            CK(cudaMemcpyAsync(g->stage_a, u, g->bytes, cudaMemcpyHostToDevice, st));
+            du = g->stage_a;
+        }
+        if (is_host_ptr(u_ref)) {
+            CK(cudaMemcpyAsync(g->stage_b, u_ref, g->bytes, cudaMemcpyHostToDevice, st));
+            dr = g->stage_b;
+        }
+    }
+    CK(cudaMemsetAsync(g->d_red, 0, 2 * sizeof(unsigned long long), st));
+    CKS(launch_maxabs(g, du, dr, g->d_red, g->d_red + 1, st));
+    CK(cudaMemcpyAsync(g->h_red, g->d_red, 2 * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const double m = bits_to_double(g->h_red[0]), M = bits_to_double(g->h_red[1]);
+    if (M == 0.0) return fail(PR_EDOMAIN, "max|u_ref| = 0: defect undefined (Eq.(defect))");
+    *d_host = m / M;
+    return PR_OK;
+}
+
+pr_status pr_fill_sine(pr_grid *g, double *u, void *stream) {
+    CKS(check_grid(g));
+    if (!u) return fail(PR_EINVAL, "null field pointer");
+    fill_sine_kernel<<<g->sms * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(g->d_sine, u, g->n);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    CKL();
+    return PR_OK;
+}
+
+static pr_status launch_correct(pr_grid *g, const double *f, const double *gn, const double *go,
+                                double *uo, const double *ref, unsigned long long *dmax,
+                                cudaStream_t st) {
+    correct_kernel<<<red_blocks(g), RED_THREADS, 0, st>>>(
+        reinterpret_cast<const double2 *>(f), reinterpret_cast<const double2 *>(gn),
+        reinterpret_cast<const double2 *>(go), reinterpret_cast<double2 *>(uo),
+        reinterpret_cast<const double2 *>(ref), dmax, g->N / 2);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    CKL();
+    return PR_OK;
+}
+
+pr_status pr_correct(pr_grid *g, const double *f, const double *g_new, const double *g_old,
+                     double *u_out, const double *u_ref, double *d_host, void *stream) {
+    CKS(check_grid(g));
+    if (!f || !g_new || !g_old || !u_out) return fail(PR_EINVAL, "null field pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const bool want = u_ref && d_host;
+    if (want) {
+        CK(cudaMemsetAsync(g->d_red, 0, 2 * sizeof(unsigned long long), st));
+        CKS(launch_maxabs(g, nullptr, u_ref, g->d_red, g->d_red + 1, st));
+    }
+    CKS(launch_correct(g, f, g_new, g_old, u_out, want ? u_ref : nullptr, g->d_red, st));
+    if (want) {
+        CK(cudaMemcpyAsync(g->h_red, g->d_red, 2 * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const double M = bits_to_double(g->h_red[1]);
+        if (M == 0.0) return fail(PR_EDOMAIN, "max|u_ref| = 0");
+        *d_host = bits_to_double(g->h_red[0]) / M;
+    }
+    return PR_OK;
+}
+
+pr_status pr_stability_ratio(const pr_problem *p, double dt, int32_t fine, double *ratio) {
+    if (!p || !ratio || p->n < 1 || !(dt > 0.0)) return fail(PR_EINVAL, "bad argument");
+    const double inv = double(p->n), numax = 1.5 * p->nu0;
+    if (fine) {
+        *ratio = dt * (16.0 * numax * inv * inv) / 2.785;
+    } else {
+        double s = 6.0 * numax * inv * inv;
+        for (int d = 0; d < 3; ++d) s += std::fabs(p->c[d]) * inv;
+        *ratio = dt * s;
+    }
+    return PR_OK;
+}
+
+// ------------------------------------------------------------------ Parareal
+pr_status pr_plan(int32_t Np, int32_t K, int32_t W, int32_t r, pr_op *ops, int32_t cap,
+                  int32_t *count) {
+    if (!count) return fail(PR_EINVAL, "count is NULL");
+    if (Np < 1 || K < 0 || W < 1 || r < 0 || r >= W || Np % W)
+        return fail(PR_EINVAL, "bad plan sizes (N_p=%d K=%d W=%d r=%d)", Np, K, W, r);
+    const int s = Np / W, j0 = r * s;
+    int c = 0;
+    auto emit = [&](int op, int k, int slice, int peer) {
+        if (ops && c < cap) ops[c] = pr_op{op, k, slice, peer};
+        ++c;
+    };
+    for (int m = 0; m < j0; ++m) emit(PR_OP_G_PREFIX, -1, m, -1);
+    for (int l = 0; l < s; ++l) emit(PR_OP_G_INIT, -1, j0 + l, -1);
+    if (r == W - 1) emit(PR_OP_DEFECT0, -1, Np - 1, -1);
+    for (int k = 0; k < K; ++k) {
+        for (int l = 0; l < s; ++l) emit(PR_OP_F, k, j0 + l, -1);
+        for (int l = 0; l < s; ++l) {
+            const int j = j0 + l;
+            if (l == 0 && j > 0) emit(PR_OP_RECV, k, j, r - 1);
+            emit(PR_OP_G, k, j, -1);
+            emit(PR_OP_CORRECT, k, j, -1);
+            if (l == s - 1 && r < W - 1) emit(PR_OP_SEND, k, j, r + 1);
+        }
+        emit(PR_OP_END_ITER, k, -1, -1);
+    }
+    *count = c;
+    return PR_OK;
+}
+
+pr_status pr_nccl_unique_id(void *id_out) {
+    if (!id_out) return fail(PR_EINVAL, "null id");
+    static_assert(sizeof(ncclUniqueId) == PR_NCCL_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(PR_ENCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+    std::memcpy(id_out, &id, sizeof id);
+    return PR_OK;
+}
+
+pr_status pr_comm_init(pr_grid *g, int32_t world, int32_t rank, const void *id) {
+    CKS(check_grid(g));
+    if (!id || world < 1 || rank < 0 || rank >= world)
+        return fail(PR_EINVAL, "bad world/rank (%d/%d)", world, rank);
+    if (g->comm) {
+        ncclCommDestroy(g->comm);
+        g->comm = nullptr;
+    }
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof uid);
+    ncclResult_t r = ncclCommInitRank(&g->comm, world, uid, rank);
+    if (r != ncclSuccess) {
+        g->comm = nullptr;
+        return fail(PR_ENCCL, "rank %d: ncclCommInitRank: %s", rank, ncclGetErrorString(r));
+    }
+    if (!g->comm_stream) CK(cudaStreamCreateWithFlags(&g->comm_stream, cudaStreamNonBlocking));
+    g->world = world;
+    g->rank = rank;
+    return PR_OK;
+}
+
+static pr_status ensure_events(pr_grid *g, size_t count) {
+    while (g->evs.size() < count) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        g->evs.push_back(e);
+    }
+    return PR_OK;
+}
+
+// Wait for `st` (and the comm stream), polling NCCL for asynchronous errors.
+static pr_status wait_all(pr_grid *g, cudaStream_t st, int k_hint) {
+    const char *tenv = getenv("PR_NCCL_TIMEOUT_S");
+    const double timeout = tenv ? atof(tenv) : 0.0;
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t ss[2] = {st, g->comm ? g->comm_stream : st};
+    for (int i = 0; i < 2; ++i) {
+        for (;;) {
+            cudaError_t e = cudaStreamQuery(ss[i]);
+            if (e == cudaSuccess) break;
+            if (e != cudaErrorNotReady)
+                return fail(PR_ECUDA, "rank %d: stream error: %s", g->rank, cudaGetErrorString(e));
+            if (g->comm) {
+                ncclResult_t ae = ncclSuccess;
+                ncclCommGetAsyncError(g->comm, &ae);
+                if (ae != ncclSuccess && ae != ncclInProgress) {
+                    ncclCommAbort(g->comm);
+                    g->comm = nullptr;
+                    return fail(PR_ENCCL, "rank %d, iteration %d: NCCL async error: %s", g->rank,
+                                k_hint, ncclGetErrorString(ae));
+                }
+                if (timeout > 0) {
+                    const double el = std::chrono::duration<double>(
+                                          std::chrono::steady_clock::now() - t0).count();
+                    if (el > timeout) {
+                        ncclCommAbort(g->comm);
+                        g->comm = nullptr;
+                        return fail(PR_ENCCL, "rank %d, iteration %d: timed out after %.1f s",
+                                    g->rank, k_hint, el);
+                    }
+                }
+            }
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+    }
+    return PR_OK;
+}
+
+#define NCK(call, k)                                                                     \
+    do {                                                                                 \
+        ncclResult_t r_ = (call);                                                        \
+        if (r_ != ncclSuccess)                                                           \
+            return fail(PR_ENCCL, "rank %d, iteration %d: %s: %s", g->rank, (k), #call,  \
+                        ncclGetErrorString(r_));                                         \
+    } while (0)
+
+pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, double *u_T,
+                      const double *u_ref, double *defects_host, void *stream) {
+    CKS(check_grid(g));
+    if (!cfg || !u0) return fail(PR_EINVAL, "null argument");
+    const int Np = cfg->n_slices, nc = cfg->n_coarse_per_slice, nf = cfg->n_fine_per_slice,
+              K = cfg->K;
+    const bool g_is_f = (cfg->flags & PR_FLAG_G_IS_F) != 0;
+    if (Np < 1 || nc < 1 || nf < 1 || K < 0)
+        return fail(PR_EINVAL, "need n_slices, N_c, N_f >= 1 and K >= 0");
+    const int W = g->comm ? g->world : 1, r = g->comm ? g->rank : 0;
+    if (g->world > 1 && !g->comm) return fail(PR_ESTATE, "world > 1 but no communicator");
+    if (Np % W) return fail(PR_EINVAL, "n_slices (%d) must be a multiple of world (%d)", Np, W);
+    const bool last = (r == W - 1);
+    if (last && !u_T) return fail(PR_EINVAL, "u_T is NULL on the last rank");
+    const int s = Np / W, j0 = r * s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const double T = g->prob.T;
+    const double Dt = T / double(int64_t(Np) * nc);  // coarse step
+    const double dt = T / double(int64_t(Np) * nf);  // fine step
+
+    std::vector<pr_op> plan;
+    int32_t cnt = 0;
+    CKS(pr_plan(Np, K, W, r, nullptr, 0, &cnt));
+    plan.resize(cnt);
+    CKS(pr_plan(Np, K, W, r, plan.data(), cnt, &cnt));
+
+    // buffers: start[s], f[s], out[s], gold[s], gnew, recv, u0d, (uref staging)
+    const size_t nbuf = size_t(4 * s + 3);
+    if (g->par_s != s || g->pool.size() != nbuf) {
+        CK(cudaDeviceSynchronize());
+        for (double *p : g->pool) CK(cudaFree(p));
+        g->pool.clear();
+        for (size_t i = 0; i < nbuf; ++i) {
+            double *p = nullptr;
+            CK(cudaMalloc(&p, g->bytes));
+            g->pool.push_back(p);
+        }
+        g->par_s = s;
+    }
+    std::vector<double *> start(s), f(s), out(s), gold(s);
+    for (int l = 0; l < s; ++l) {
+        start[l] = g->pool[l];
+        f[l] = g->pool[s + l];
+        out[l] = g->pool[2 * s + l];
+        gold[l] = g->pool[3 * s + l];
+    }
+    double *gnew = g->pool[4 * s], *recvb = g->pool[4 * s + 1], *u0d = g->pool[4 * s + 2];
+    const bool want_def = last && u_ref && defects_host;
+    const double *refd = u_ref;
+    if (want_def && is_host_ptr(u_ref)) {
+        CKS(ensure_stage(g));
+        CK(cudaMemcpyAsync(g->stage_b, u_ref, g->bytes, cudaMemcpyHostToDevice, st));
+        refd = g->stage_b;
+    }
+    CKS(ensure_red(g, K + 2));
+    // events: 0 start, 1 init done, then per iteration 4: F done, recv done (compute), iter done, send done
+    CKS(ensure_events(g, size_t(2 + 4 * K + 2)));
+    cudaEvent_t ev_start = g->evs[0], ev_init = g->evs[1];
+    auto evF = [&](int k) { return g->evs[2 + 4 * k]; };
+    auto evW = [&](int k) { return g->evs[3 + 4 * k]; };
+    auto evI = [&](int k) { return g->evs[4 + 4 * k]; };
+    auto evS = [&](int k) { return g->evs[5 + 4 * k]; };
+    std::vector<cudaEvent_t> recv_ev(K), corr_ev(K);
+    // timing-free events for the cross-stream dependencies
+    std::vector<cudaEvent_t> &dep = g->dep_evs;
+    while (dep.size() < size_t(2 * K + 2)) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        dep.push_back(e);
+    }
+    for (int k = 0; k < K; ++k) {
+        recv_ev[k] = dep[2 * k];
+        corr_ev[k] = dep[2 * k + 1];
+    }
+    cudaEvent_t fdone_ev = dep[2 * K];
+
+    CK(cudaEventRecord(ev_start, st));
+    if (is_host_ptr(u0))
+        CK(cudaMemcpyAsync(u0d, u0, g->bytes, cudaMemcpyHostToDevice, st));
+    else
+        CK(cudaMemcpyAsync(u0d, u0, g->bytes, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemsetAsync(g->d_red, 0, size_t(K + 2) * sizeof(unsigned long long), st));
+    // nu tables for everything this rank will run (one upload each)
+    if (g_is_f) {
+        CKS(ensure_table(g, 1, dt, 0, int64_t(j0 + s) * nf, st));
+    } else {
+        CKS(ensure_table(g, 1, dt, int64_t(j0) * nf, int64_t(j0 + s) * nf, st));
+        CKS(ensure_table(g, 0, Dt, 0, int64_t(j0 + s) * nc, st));
+    }
+    // slots: d_red[k] = max|u^k_{N_p} - u_ref| (k = 0..K), d_red[K+1] = max|u_ref|
+    if (want_def) CKS(launch_maxabs(g, nullptr, refd, nullptr, g->d_red + K + 1, st));
+
+    auto G = [&](const double *in, double *o, int m) -> pr_status {
+        if (g_is_f) return run_fine(g, in, o, int64_t(m) * nf, nf, dt, st);
+        return run_coarse(g, in, o, int64_t(m) * nc, nc, Dt, st);
+    };
+    auto Fp = [&](const double *in, double *o, int m) -> pr_status {
+        return run_fine(g, in, o, int64_t(m) * nf, nf, dt, st);
+    };
+
+    const double *v = u0d;
+    bool sent_pending = false;
+    int last_send_k = -1;
+    float ms_fine = 0, ms_wait = 0, ms_gc = 0;
+    bool init_marked = false;
+    for (const pr_op &op : plan) {
+        const int l = op.slice - j0;
+        if (op.k >= 0 && !init_marked) {
+            CK(cudaEventRecord(ev_init, st));
+            init_marked = true;
+        }
+        switch (op.op) {
+        case PR_OP_G_PREFIX:
+            CKS(G(v, start[0], op.slice));
+            v = start[0];
+            break;
+        case PR_OP_G_INIT:
+            if (op.slice == 0) {
+                start[0] = u0d;  // rank 0 keeps u0 as its start value
+            } else if (start[l] != v) {
+                CK(cudaMemcpyAsync(start[l], v, g->bytes, cudaMemcpyDeviceToDevice, st));
+            }
+            CKS(G(start[l], gold[l], op.slice));
+            v = gold[l];
+            break;
+        case PR_OP_DEFECT0:  // d^0: coarse initial guess at T vs u_ref (C11)
+            if (want_def) CKS(launch_maxabs(g, gold[s - 1], refd, g->d_red + 0, nullptr, st));
+            break;
+        case PR_OP_F:
+            CKS(Fp(start[l], f[l], op.slice));
+            if (l == s - 1) {
+                CK(cudaEventRecord(evF(op.k), st));
+                CK(cudaEventRecord(fdone_ev, st));
+            }
+            break;
+        case PR_OP_RECV:
+            // the receive buffer was last read by F of iteration k-1 (done: stream order)
+            CK(cudaStreamWaitEvent(g->comm_stream, fdone_ev, 0));
+            NCK(ncclRecv(recvb, size_t(g->N), ncclDouble, op.peer, g->comm, g->comm_stream), op.k);
+            CK(cudaEventRecord(recv_ev[op.k], g->comm_stream));
+            CK(cudaStreamWaitEvent(st, recv_ev[op.k], 0));
+            break;
+        case PR_OP_G: {
+            const double *in;
+            if (op.slice == 0) in = u0d;
+            else if (l == 0) in = recvb;
+            else in = out[l - 1];
+            if (l == 0) CK(cudaEventRecord(evW(op.k), st));
+            CKS(G(in, gnew, op.slice));
+            break;
+        }
+        case PR_OP_CORRECT: {
+            if (l == s - 1 && sent_pending) {  // out[s-1] still being sent from iteration k-1
+                CK(cudaStreamWaitEvent(st, evS(last_send_k), 0));
+                sent_pending = false;
+            }
+            const bool fuse = want_def && op.slice == Np - 1;
+            CKS(launch_correct(g, f[l], gnew, gold[l], out[l], fuse ? refd : nullptr,
+                               g->d_red + op.k + 1, st));
+            std::swap(gold[l], gnew);
+            break;
+        }
+        case PR_OP_SEND:
+            CK(cudaEventRecord(corr_ev[op.k], st));
+            CK(cudaStreamWaitEvent(g->comm_stream, corr_ev[op.k], 0));
+            NCK(ncclSend(out[s - 1], size_t(g->N), ncclDouble, op.peer, g->comm, g->comm_stream),
+                op.k);
+            CK(cudaEventRecord(evS(op.k), g->comm_stream));
+            sent_pending = true;
+            last_send_k = op.k;
+            break;
+        case PR_OP_END_ITER:
+            CK(cudaEventRecord(evI(op.k), st));
+            // start[l] <- the input slice l used in this iteration (buffer rotation)
+            for (int ll = s - 1; ll >= 1; --ll) std::swap(start[ll], out[ll - 1]);
+            if (j0 > 0) std::swap(start[0], recvb);
+            break;
+        default:
+            return fail(PR_EINVAL, "bad plan op %d", op.op);
+        }
+    }
+    if (!init_marked) CK(cudaEventRecord(ev_init, st));
+    if (last) {
+        const double *res = K > 0 ? out[s - 1] : gold[s - 1];
+        // after END_ITER the final output of the last slice is still out[s-1]
+        CK(cudaMemcpyAsync(u_T, res, g->bytes,
+                           is_host_ptr(u_T) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st));
+        if (want_def)
+            CK(cudaMemcpyAsync(g->h_red, g->d_red, size_t(K + 2) * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, st));
+    }
+    cudaEvent_t ev_end = g->evs[2 + 4 * K];
+    CK(cudaEventRecord(ev_end, st));
+    CKS(wait_all(g, st, K - 1));
+    if (want_def) {
+        const double M = bits_to_double(g->h_red[K + 1]);
+        if (M == 0.0) return fail(PR_EDOMAIN, "max|u_ref| = 0: defect undefined");
+        for (int k = 0; k <= K; ++k) defects_host[k] = bits_to_double(g->h_red[k]) / M;
+    }
+    // timings
+    float tot = 0, init = 0;
+    cudaEventElapsedTime(&tot, ev_start, ev_end);
+    cudaEventElapsedTime(&init, ev_start, ev_init);
+    for (int k = 0; k < K; ++k) {
+        float a = 0, b = 0, c = 0;
+        cudaEvent_t prev = k == 0 ? ev_init : evI(k - 1);
+        cudaEventElapsedTime(&a, prev, evF(k));
+        cudaEventElapsedTime(&b, evF(k), evW(k));
+        cudaEventElapsedTime(&c, evW(k), evI(k));
+        ms_fine += a;
+        ms_wait += b;
+        ms_gc += c;
+    }
+    g->timings[0] = tot;
+    g->timings[1] = init;
+    g->timings[2] = ms_fine;
+    g->timings[3] = ms_wait;
+    g->timings[4] = ms_gc;
+    return PR_OK;
+}
+
+pr_status pr_last_timings(pr_grid *g, double *out, int32_t cap) {
+    if (!g || !out || cap < 5) return fail(PR_EINVAL, "bad argument");
+    for (int i = 0; i < 5; ++i) out[i] = g->timings[i];
+    return PR_OK;
+}
+
+}  // extern "C"

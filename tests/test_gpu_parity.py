@@ -1,0 +1,228 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same
+seeded inputs.  Tolerance (north_star; C13/C14): normwise
+max|gpu - oracle| / max|oracle| <= 1e-12 on fields, |d_gpu - d_oracle| <= 1e-10
+on defects.  Sizes span several tiles (32 x 16 in x, y; z chunks) and ragged
+tails (n = 40, 48), non-powers of two (12), tiny grids whose tile wraps the
+domain several times (n = 4, 8), and the full BASELINE sizes on a few steps."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle
+import paper_1409_8563_b200 as pr
+from synthetic import random_field, PARITY_C
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def rel(a, b):
+    a = a.cpu().numpy() if hasattr(a, "cpu") else a
+    return float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+_grids = {}
+
+
+def grid(n, c=PARITY_C, nu0=0.1, omega=100.0, T=0.1, nu_mode=0):
+    key = (n, tuple(c), nu0, omega, T, nu_mode)
+    if key not in _grids:
+        _grids[key] = pr.Grid(pr.Problem(n, c=c, nu0=nu0, omega=omega, T=T, nu_mode=nu_mode))
+    return _grids[key]
+
+
+def oproblem(n, c=PARITY_C, nu0=0.1, omega=100.0, T=0.1, nu_mode=0):
+    return oracle.Problem(n, c=c, nu0=nu0, omega=omega, T=T, nu_mode=nu_mode)
+
+
+@pytest.mark.parametrize("n", [4, 8, 12, 32, 40, 48, 64])
+@pytest.mark.parametrize("nu_mode", [0, 1])
+def test_fine_steps(n, nu_mode):
+    u0 = random_field(n, 0)
+    g = grid(n, nu_mode=nu_mode)
+    dt = 2e-4 * (32 / n) ** 2
+    for step0, steps in ((0, 1), (7, 3), (100, 21)):  # 21 > one 16-step graph + remainder
+        out = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+        pr.pr_fine(g, dev(u0), out, step0, steps, dt)
+        ref = oracle.fine(oproblem(n, nu_mode=nu_mode), u0, step0, steps, dt)
+        assert rel(out, ref) <= TOL, (n, step0, steps)
+
+
+@pytest.mark.parametrize("n", [4, 8, 12, 32, 40, 48, 64])
+def test_coarse_steps(n):
+    u0 = random_field(n, 1)
+    g = grid(n)
+    Dt = 5e-4 * (32 / n) ** 2
+    for step0, steps in ((0, 1), (3, 2), (5, 7), (9, 40), (0, 33)):
+        out = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+        pr.pr_coarse(g, dev(u0), out, step0, steps, Dt)
+        ref = oracle.coarse(oproblem(n), u0, step0, steps, Dt)
+        assert rel(out, ref) <= TOL, (n, step0, steps)
+
+
+@pytest.mark.parametrize("which", ["fine", "coarse"])
+@pytest.mark.parametrize("steps", [0, 1, 2, 5, 34])
+def test_in_place_and_zero_steps(which, steps):
+    n = 32
+    u0 = random_field(n, 2)
+    g = grid(n)
+    dt = 1e-4
+    fn = pr.pr_fine if which == "fine" else pr.pr_coarse
+    ofn = oracle.fine if which == "fine" else oracle.coarse
+    u = dev(u0)
+    fn(g, u, u, 11, steps, dt)
+    ref = ofn(oproblem(n), u0, 11, steps, dt)
+    if steps == 0:
+        assert np.array_equal(u.cpu().numpy(), u0)
+    else:
+        assert rel(u, ref) <= TOL
+
+
+@pytest.mark.parametrize("c", [(1.0, 1.0, 1.0), (-1.0, -0.5, 0.0), (0.0, 0.0, 0.0), (0.3, -2.0, 1.5)])
+def test_velocity_signs(c):
+    """Both upwind branches and c_a = 0 (strict > test, C4)."""
+    n = 32
+    u0 = random_field(n, 3)
+    g = grid(n, c=c)
+    for which, fn, ofn, dt in (("f", pr.pr_fine, oracle.fine, 1e-4), ("g", pr.pr_coarse, oracle.coarse, 4e-4)):
+        out = torch.empty_like(dev(u0))
+        fn(g, dev(u0), out, 0, 5, dt)
+        assert rel(out, ofn(oproblem(n, c=c), u0, 0, 5, dt)) <= TOL, which
+
+
+def test_host_pointers():
+    """pr_fine / pr_coarse / pr_defect accept host buffers (staged internally)."""
+    n = 32
+    u0 = random_field(n, 4)
+    g = grid(n)
+    out = np.empty_like(u0)
+    pr.pr_fine(g, u0, out, 3, 4, 1e-4)
+    assert rel(out, oracle.fine(oproblem(n), u0, 3, 4, 1e-4)) <= TOL
+    pr.pr_coarse(g, u0, out, 3, 5, 4e-4)
+    assert rel(out, oracle.coarse(oproblem(n), u0, 3, 5, 4e-4)) <= TOL
+    v = random_field(n, 5)
+    assert abs(pr.pr_defect(g, v, u0) - oracle.defect(v, u0)) <= 1e-15
+
+
+def test_fill_sine_defect_correct():
+    n = 48
+    g = grid(n)
+    u = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+    pr.pr_fill_sine(g, u)
+    assert rel(u, oracle.initial(n)) <= 1e-15
+    a, b, c, r = (random_field(n, s) for s in (6, 7, 8, 9))
+    out = torch.empty_like(u)
+    d = pr.pr_correct(g, dev(a), dev(b), dev(c), out, dev(r))
+    exp = a + (b - c)
+    assert np.array_equal(out.cpu().numpy(), exp)  # elementwise, C5 order: bitwise
+    assert d == oracle.defect(exp, r)
+    assert pr.pr_defect(g, dev(a), dev(r)) == oracle.defect(a, r)
+    bad = dev(a)
+    bad[3, 4, 5] = float("nan")
+    assert np.isnan(pr.pr_defect(g, bad, dev(r)))
+    with pytest.raises(pr.PrError) as e:
+        pr.pr_defect(g, dev(a), torch.zeros_like(u))
+    assert e.value.status == 5  # PR_EDOMAIN
+
+
+def test_errors():
+    g = grid(32)
+    u = torch.zeros((32, 32, 32), dtype=torch.float64, device="cuda")
+    with pytest.raises(pr.PrError):
+        pr.pr_fine(g, u, u, 0, -1, 1e-4)
+    with pytest.raises(pr.PrError):
+        pr.pr_fine(g, u, u, 0, 1, 0.0)
+    big = torch.zeros(2 * 32 ** 3, dtype=torch.float64, device="cuda")
+    with pytest.raises(pr.PrError):  # overlapping but not identical
+        pr.pr_coarse(g, big[:32 ** 3], big[8:8 + 32 ** 3], 0, 1, 1e-4)
+    for bad in (pr.PararealCfg(0, 2, 2, 1), pr.PararealCfg(2, 0, 2, 1), pr.PararealCfg(2, 2, 2, -1)):
+        with pytest.raises(pr.PrError) as e:
+            pr.pr_parareal(g, bad, u, u)
+        assert e.value.status == 1  # PR_EINVAL
+
+
+# ----------------------------------------------------------------- Parareal
+def cfg1_oracle(nu_mode):
+    n, Nt, NC, Np, K = 32, 2048, 128, 4, 2
+    p = oracle.Problem(n, nu_mode=nu_mode)
+    u0 = oracle.initial(n)
+    uf = oracle.serial_fine(p, Nt, u0)
+    res = oracle.parareal(p, Np, NC // Np, Nt // Np, K, u0, uf)
+    return p, u0, uf, res
+
+
+@pytest.fixture(scope="module")
+def cfg1_ref():
+    return {m: cfg1_oracle(m) for m in (0, 1)}
+
+
+@pytest.mark.parametrize("nu_mode", [0, 1])
+def test_parareal_cfg1(cfg1_ref, nu_mode):
+    """BASELINE configs[0]: 32^3, 4 slices, K=2 on one GPU (slice group s = 4)."""
+    p, u0, uf, res = cfg1_ref[nu_mode]
+    g = grid(32, c=(1.0, 1.0, 1.0), nu_mode=nu_mode)
+    uf_g = torch.empty((32, 32, 32), dtype=torch.float64, device="cuda")
+    pr.pr_fine(g, dev(u0), uf_g, 0, 2048, 0.1 / 2048)
+    assert rel(uf_g, uf) <= TOL
+    uT = torch.empty_like(uf_g)
+    d = pr.pr_parareal(g, pr.PararealCfg(4, 32, 512, 2), dev(u0), uT, dev(uf))
+    assert rel(uT, res.u_T) <= TOL
+    assert np.max(np.abs(np.array(d) - res.defects)) <= 1e-10
+    # host buffers through the same call (the e2e path)
+    uT_h = np.empty_like(u0)
+    d_h = pr.pr_parareal(g, pr.PararealCfg(4, 32, 512, 2), u0, uT_h, uf)
+    assert np.array_equal(uT_h, uT.cpu().numpy()) and d_h == d
+
+
+def test_parareal_exactness_and_degenerate():
+    """K = N_p: u_T equals the GPU serial fine run bitwise (C5 + C6); G = F: d^1 = 0."""
+    n, Np, nc, nf = 32, 4, 8, 32
+    g = grid(n, T=0.01)
+    u0 = dev(random_field(n, 12))
+    uf = torch.empty_like(u0)
+    pr.pr_fine(g, u0, uf, 0, Np * nf, 0.01 / (Np * nf))
+    uT = torch.empty_like(u0)
+    d = pr.pr_parareal(g, pr.PararealCfg(Np, nc, nf, Np), u0, uT, uf)
+    assert torch.equal(uT, uf) and d[Np] == 0.0
+    d = pr.pr_parareal(g, pr.PararealCfg(Np, nc, nf, 2, flags=pr.PR_FLAG_G_IS_F), u0, uT, uf)
+    assert d[1] == 0.0 and d[2] == 0.0
+    # K = 0: the coarse initial guess
+    d = pr.pr_parareal(g, pr.PararealCfg(Np, nc, nf, 0), u0, uT, uf)
+    ug = torch.empty_like(u0)
+    pr.pr_coarse(g, u0, ug, 0, Np * nc, 0.01 / (Np * nc))
+    assert torch.equal(uT, ug)
+
+
+def test_parareal_small_random_vs_oracle():
+    n, Np, nc, nf, K = 12, 3, 3, 10, 2
+    p = oracle.Problem(n, c=PARITY_C, T=0.004)
+    u0 = random_field(n, 13)
+    uf = oracle.serial_fine(p, Np * nf, u0)
+    ref = oracle.parareal(p, Np, nc, nf, K, u0, uf)
+    g = grid(n, T=0.004)
+    uT = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+    d = pr.pr_parareal(g, pr.PararealCfg(Np, nc, nf, K), dev(u0), uT, dev(uf))
+    assert rel(uT, ref.u_T) <= TOL
+    assert np.max(np.abs(np.array(d) - ref.defects)) <= 1e-10
+
+
+# ---------------------------------------------------------- full BASELINE sizes
+@pytest.mark.parametrize("n", [128, 256])
+def test_full_size_steps_vs_oracle(n):
+    """Launch configuration bench.py times, a few steps, all n^3 outputs."""
+    u0 = random_field(n, 20)
+    g = grid(n, c=(1.0, 1.0, 1.0))
+    p = oproblem(n, c=(1.0, 1.0, 1.0))
+    dt, Dt = 0.1 / 2 ** 17 * (256 / n) ** 2, 0.1 / 2 ** 13 * (256 / n) ** 2
+    out = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+    pr.pr_fine(g, dev(u0), out, 1000, 2, dt)
+    assert rel(out, oracle.fine(p, u0, 1000, 2, dt)) <= TOL
+    pr.pr_coarse(g, dev(u0), out, 500, 3, Dt)
+    assert rel(out, oracle.coarse(p, u0, 500, 3, Dt)) <= TOL
