@@ -67,4 +67,6 @@ CONFIGS = {
     "cfg5": Config("cfg5", 256, 0.1, 2 ** 17, 2 ** 13, 8, 3),
     # bench workload: cfg3 shortened 16x in T with the same dt and Dt.
     "cfg3s": Config("cfg3s", 256, 0.1 / 16, 2 ** 13, 2 ** 9, 8, 3),
+    # profiling variant: cfg3's dt and Dt, 512x shorter (launch lists under ncu).
+    "cfg3p": Config("cfg3p", 256, 0.1 / 512, 2 ** 8, 2 ** 4, 8, 3),
 }
