@@ -15,9 +15,9 @@
 // Stencil kernels: a CTA owns an (x,y) tile of TX x TY points and marches a
 // chunk of z planes.  Each plane of the stencil input (with a 2-point x halo
 // and an R-point y halo, wrapped periodically) and each plane of the
-// pointwise inputs is fetched by the TMA bulk-copy engine
-// (cp.async.bulk ... mbarrier::complete_tx) into a DEPTH-slot shared-memory
-// ring, several planes ahead of the compute.  z neighbours live in a per-thread
+// pointwise inputs is fetched with 16-byte asynchronous copies (cp.async,
+// every thread issuing its share) into a DEPTH-slot shared-memory ring,
+// several planes ahead of the compute.  z neighbours live in a per-thread
 // register queue; x/y neighbours are read from the current shared-memory
 // plane.  Outputs are written straight to global memory, coalesced along x.
 #pragma once
@@ -29,13 +29,20 @@ namespace prk {
 enum Kind { K_COARSE = 0, K_S1 = 1, K_S2 = 2, K_S3 = 3, K_S4 = 4 };
 
 constexpr int TX = 32;            // tile width (one warp along x)
-constexpr int TY = 16;            // tile height
-constexpr int RPT = 4;            // consecutive y rows per thread
-constexpr int BY = TY / RPT;      // thread rows per CTA
-constexpr int NTHREADS = TX * BY; // 128
-constexpr int HX = 2;             // x halo kept in smem (2 => 16-byte aligned rows)
+constexpr int HX = 2;             // x halo kept in smem (2 => 16-byte aligned chunks)
 constexpr int SX = TX + 2 * HX;   // smem row stride in doubles (36)
-constexpr int DEPTH = 6;          // ring slots (planes in flight + in use)
+
+// Tile variants: TY rows per tile, RPT consecutive rows per thread, DEPTH ring slots.
+template <int TY_, int RPT_, int DEPTH_> struct TileCfg {
+    static constexpr int TY = TY_, RPT = RPT_, DEPTH = DEPTH_;
+    static constexpr int BY = TY / RPT;
+    static constexpr int NTHREADS = TX * BY;
+    static_assert(TY % RPT == 0, "TY must be a multiple of RPT");
+};
+using Tile0 = TileCfg<16, 4, 7>;   // 128 threads
+using Tile1 = TileCfg<16, 2, 7>;   // 256 threads
+using Tile2 = TileCfg<32, 4, 6>;   // 256 threads, larger tile (less halo re-read)
+using Tile3 = TileCfg<8, 2, 8>;    // 128 threads, small slots (3-4 CTAs/SM)
 
 template <int KIND> struct Traits;
 template <> struct Traits<K_COARSE> { static constexpr int R = 1, NP = 0; };
@@ -44,12 +51,15 @@ template <> struct Traits<K_S2> { static constexpr int R = 2, NP = 2; };  // Ya*
 template <> struct Traits<K_S3> { static constexpr int R = 2, NP = 2; };  // Yb*, u, acc
 template <> struct Traits<K_S4> { static constexpr int R = 2, NP = 1; };  // Ya*, acc
 
-template <int KIND> struct Layout {
+template <int KIND, class C> struct Layout {
     static constexpr int R = Traits<KIND>::R, NP = Traits<KIND>::NP;
-    static constexpr int Y_ELEMS = (TY + 2 * R) * SX;   // stencil plane with halos
-    static constexpr int P_ELEMS = TY * TX;             // one pointwise plane
+    static constexpr int Y_ROWS = C::TY + 2 * R;
+    static constexpr int Y_ELEMS = Y_ROWS * SX;          // stencil plane with halos
+    static constexpr int P_ELEMS = C::TY * TX;           // one pointwise plane
     static constexpr int SLOT_ELEMS = Y_ELEMS + NP * P_ELEMS;
-    static constexpr size_t SMEM_BYTES = size_t(DEPTH) * SLOT_ELEMS * sizeof(double);
+    static constexpr size_t SMEM_BYTES = size_t(C::DEPTH) * SLOT_ELEMS * sizeof(double);
+    static constexpr int Y_CHUNKS = Y_ROWS * (SX / 2);   // 16-byte chunks, full tile
+    static constexpr int P_CHUNKS = NP * C::TY * (TX / 2);
 };
 
 struct StencilArgs {
@@ -72,37 +82,16 @@ struct StencilArgs {
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+// 16-byte global -> shared asynchronous copy (LDGSTS), L1 bypass
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
-                                         uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ int wrapi(int i, int n) {
@@ -110,87 +99,93 @@ __device__ __forceinline__ int wrapi(int i, int n) {
     return i < 0 ? i + n : i;
 }
 
-// Issue the bulk copies of stream element e (plane z_begin - R + e) into its
-// ring slot.  Executed by all 32 lanes of warp 0.
-template <int KIND>
-__device__ __forceinline__ void issue_element(const StencilArgs &a, double *ring, uint64_t *bars,
-                                              int e, int z_begin, int nz, int x0, int w, int y0,
-                                              int h, int lane) {
-    using L = Layout<KIND>;
+// Issue the 16-byte copies of stream element e (plane z_begin - R + e) into
+// its ring slot: every thread takes every NTHREADS-th chunk.  Periodic wrap is
+// applied per chunk (n even => a chunk never straddles the wrap).
+template <int KIND, class C>
+__device__ __forceinline__ void issue_element(const StencilArgs &a, double *ring, int e,
+                                              int z_begin, int nz, int x0, int w, int y0,
+                                              int h) {
+    using L = Layout<KIND, C>;
     constexpr int R = L::R, NP = L::NP;
     const int n = a.n;
-    const int slot = e % DEPTH;
-    double *ys = ring + size_t(slot) * L::SLOT_ELEMS;
+    double *ys = ring + size_t(e % C::DEPTH) * L::SLOT_ELEMS;
     const int z = wrapi(z_begin - R + e, n);
     const bool pw = NP > 0 && e >= R && e < nz + R;
-    const int yrows = h + 2 * R;
-    const uint32_t bytes = uint32_t(yrows) * uint32_t(w + 2 * HX) * 8u +
-                           (pw ? uint32_t(NP) * uint32_t(h) * uint32_t(w) * 8u : 0u);
-    if (lane == 0) mbar_arrive_expect_tx(&bars[slot], bytes);
-    __syncwarp();
     const size_t plane = size_t(z) * n * n;
-    for (int r = lane; r < yrows; r += 32) {
-        const int yy = wrapi(y0 - R + r, n);
-        const double *row = a.y + plane + size_t(yy) * n;
-        double *dst = ys + r * SX;
-        int s = x0 - HX, left = w + 2 * HX, off = 0;
-        while (left > 0) {  // periodic pieces of [x0-2, x0+w+2)
-            const int src = wrapi(s, n);
-            const int m = min(left, n - src);
-            bulk_g2s(dst + off, row + src, uint32_t(m) * 8u, &bars[slot]);
-            s += m; off += m; left -= m;
+    if (w == TX && h == C::TY) {  // full tile: compile-time chunk decomposition
+        constexpr int CW = SX / 2;
+        for (int c = threadIdx.x; c < L::Y_CHUNKS; c += C::NTHREADS) {
+            const int r = c / CW, cc = c % CW;
+            int yy = y0 - R + r;
+            yy += (yy < 0) ? n : 0;
+            yy -= (yy >= n) ? n : 0;
+            int xs = x0 - HX + 2 * cc;
+            xs += (xs < 0) ? n : 0;
+            xs -= (xs >= n) ? n : 0;
+            cp_async16(ys + r * SX + 2 * cc, a.y + plane + size_t(yy) * n + xs);
         }
-    }
-    if (pw) {
-        const int zz = z;  // pointwise planes are never wrapped (R <= e < nz+R)
-        for (int q = lane; q < NP * h; q += 32) {
-            const int f = q / h, r = q % h;
-            const double *src = (f == 0 ? a.p0 : a.p1) + size_t(zz) * n * n + size_t(y0 + r) * n + x0;
-            double *dst = ys + L::Y_ELEMS + f * L::P_ELEMS + r * TX;
-            bulk_g2s(dst, src, uint32_t(w) * 8u, &bars[slot]);
+        if (pw) {
+            constexpr int PC = C::TY * (TX / 2);
+            for (int c = threadIdx.x; c < L::P_CHUNKS; c += C::NTHREADS) {
+                const int f = c / PC, rem = c % PC, r = rem / (TX / 2), cc = rem % (TX / 2);
+                const double *src = (f == 0 ? a.p0 : a.p1) + plane + size_t(y0 + r) * n + x0 + 2 * cc;
+                cp_async16(ys + L::Y_ELEMS + f * L::P_ELEMS + r * TX + 2 * cc, src);
+            }
+        }
+    } else {  // ragged or wrapped tile (n not a multiple of the tile, or n < TX)
+        const int cw = (w + 2 * HX) / 2, yrows = h + 2 * R;
+        for (int c = threadIdx.x; c < yrows * cw; c += C::NTHREADS) {
+            const int r = c / cw, cc = c % cw;
+            const int yy = wrapi(y0 - R + r, n), xs = wrapi(x0 - HX + 2 * cc, n);
+            cp_async16(ys + r * SX + 2 * cc, a.y + plane + size_t(yy) * n + xs);
+        }
+        if (pw) {
+            const int pcw = w / 2, pc = h * pcw;
+            for (int c = threadIdx.x; c < NP * pc; c += C::NTHREADS) {
+                const int f = c / pc, rem = c % pc, r = rem / pcw, cc = rem % pcw;
+                const double *src = (f == 0 ? a.p0 : a.p1) + plane + size_t(y0 + r) * n + x0 + 2 * cc;
+                cp_async16(ys + L::Y_ELEMS + f * L::P_ELEMS + r * TX + 2 * cc, src);
+            }
         }
     }
 }
 
-template <int KIND>
-__global__ void __launch_bounds__(NTHREADS)
+// One fused stencil pass.  Stream elements e = 0 .. nz+2R-1 are the planes
+// z_begin-R .. z_begin+nz+R-1 (periodic in z); the pointwise planes ride along
+// with elements R .. nz+R-1.  Iteration i computes plane z_begin+i from the
+// x/y neighbours in element i+R and the z queue (elements i..i+2R).
+template <int KIND, class C>
+__global__ void __launch_bounds__(C::NTHREADS)
 stencil_kernel(const StencilArgs a) {
-    using L = Layout<KIND>;
-    constexpr int R = L::R, NP = L::NP, Q = 2 * R + 1;
+    using L = Layout<KIND, C>;
+    constexpr int R = L::R, Q = 2 * R + 1, RPT = C::RPT, DEPTH = C::DEPTH;
+    static_assert(DEPTH >= 2 * R + 2, "ring too shallow");
     extern __shared__ __align__(128) double ring[];
-    __shared__ __align__(8) uint64_t bars[DEPTH];
 
     const int n = a.n;
     int b = blockIdx.x;
     const int tix = b % a.tiles_x; b /= a.tiles_x;
     const int tiy = b % a.tiles_y; b /= a.tiles_y;
     const int cz = b;
-    const int x0 = tix * TX, y0 = tiy * TY;
-    const int w = min(TX, n - x0), h = min(TY, n - y0);
+    const int x0 = tix * TX, y0 = tiy * C::TY;
+    const int w = min(TX, n - x0), h = min(C::TY, n - y0);
     const int z_begin = cz * a.cz;
     const int nz = min(a.cz, n - z_begin);
     const int E = nz + 2 * R;
 
     const int tx = threadIdx.x % TX;
     const int ty = threadIdx.x / TX;
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int row0 = ty * RPT;  // first tile row of this thread
 
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < DEPTH; ++s) mbar_init(&bars[s], 1);
-        fence_mbar_init();
+    // prologue: DEPTH elements in flight, one commit group each
+    for (int e = 0; e < DEPTH; ++e) {
+        if (e < E) issue_element<KIND, C>(a, ring, e, z_begin, nz, x0, w, y0, h);
+        cp_async_commit();
     }
-    __syncthreads();
+    int e_next = DEPTH;
 
-    int e_next = 0;
-    if (warp == 0) {
-        for (; e_next < DEPTH && e_next < E; ++e_next)
-            issue_element<KIND>(a, ring, bars, e_next, z_begin, nz, x0, w, y0, h, lane);
-    } else {
-        e_next = min(DEPTH, E);
-    }
-
-    // Coefficients (read after the prologue copies are in flight).
+    // Coefficients (read while the prologue copies are in flight).
     const double nu = a.nu_tab[(*a.nu_pos + a.j_local) * (KIND == K_COARSE ? 1 : 4) +
                                (KIND == K_COARSE ? 0 : KIND - 1)];
     // Per-neighbour weights of the folded operator: L = w0 y + sum_a sum_o w_{a,o} y_{+o e_a}
@@ -222,29 +217,37 @@ stencil_kernel(const StencilArgs a) {
         }
     }
     const double dt = a.dt;
-
     const bool col_ok = tx < w;
+
     double q[RPT][Q];  // z queue: q[r][R + o] = Y(z + o) at (x, row0 + r)
+    // initial queue fill from elements 0 .. 2R-1
+    cp_async_wait<DEPTH - 2 * R>();
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 2 * R; ++e) {
+        const double *ys = ring + size_t(e % DEPTH) * L::SLOT_ELEMS;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) q[r][e] = ys[(R + row0 + r) * SX + HX + tx];
+    }
 
     for (int i = 0; i < nz; ++i) {
-        if (i == 0) {
-            for (int e = 0; e < 2 * R; ++e) {
-                mbar_wait(&bars[e % DEPTH], (e / DEPTH) & 1);
-                const double *ys = ring + size_t(e % DEPTH) * L::SLOT_ELEMS;
-#pragma unroll
-                for (int r = 0; r < RPT; ++r)
-                    q[r][e] = ys[(R + row0 + r) * SX + HX + tx];
-            }
+        // own copies of element i+2R have landed ...
+        if (i + R + 1 >= DEPTH) cp_async_wait<DEPTH - R - 2>();
+        else cp_async_wait<DEPTH - 1 - 2 * R>();
+        // ... and everyone's; every read of element i-1+R (and older) is done
+        __syncthreads();
+        while (e_next < E && e_next - DEPTH <= i - 1 + R) {
+            issue_element<KIND, C>(a, ring, e_next, z_begin, nz, x0, w, y0, h);
+            ++e_next;
         }
+        cp_async_commit();
+
         {
-            const int e = i + 2 * R;
-            mbar_wait(&bars[e % DEPTH], (e / DEPTH) & 1);
-            const double *ys = ring + size_t(e % DEPTH) * L::SLOT_ELEMS;
+            const double *ys = ring + size_t((i + 2 * R) % DEPTH) * L::SLOT_ELEMS;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) q[r][2 * R] = ys[(R + row0 + r) * SX + HX + tx];
         }
-        const int ec = i + R;  // element holding the centre plane
-        const double *ys = ring + size_t(ec % DEPTH) * L::SLOT_ELEMS;
+        const double *ys = ring + size_t((i + R) % DEPTH) * L::SLOT_ELEMS;
         const double *ps = ys + L::Y_ELEMS;
         const int z = z_begin + i;
 
@@ -252,12 +255,8 @@ stencil_kernel(const StencilArgs a) {
         double col[RPT + 2 * R];
 #pragma unroll
         for (int r = 0; r < RPT + 2 * R; ++r) {
-            if (r >= R && r < R + RPT) continue;
-            col[r] = ys[(row0 + r) * SX + HX + tx];
-        }
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-            col[R + r] = q[r][R];
+            if (r >= R && r < R + RPT) col[r] = q[r - R][R];
+            else col[r] = ys[(row0 + r) * SX + HX + tx];
         }
 
 #pragma unroll
@@ -265,23 +264,22 @@ stencil_kernel(const StencilArgs a) {
             const int row = row0 + r;
             const double *yrow = ys + (R + row) * SX + HX + tx;
             const double yc = q[r][R];
-            double acc = w0 * yc;
-            // x neighbours
-            if constexpr (R == 2) acc = fma(wm2[0], yrow[-2], acc);
-            acc = fma(wm1[0], yrow[-1], acc);
-            acc = fma(wp1[0], yrow[1], acc);
-            if constexpr (R == 2) acc = fma(wp2[0], yrow[2], acc);
-            // y neighbours (col index R + r is the centre)
-            if constexpr (R == 2) acc = fma(wm2[1], col[r + R - 2], acc);
-            acc = fma(wm1[1], col[r + R - 1], acc);
-            acc = fma(wp1[1], col[r + R + 1], acc);
-            if constexpr (R == 2) acc = fma(wp2[1], col[r + R + 2], acc);
-            // z neighbours from the queue
-            if constexpr (R == 2) acc = fma(wm2[2], q[r][R - 2], acc);
-            acc = fma(wm1[2], q[r][R - 1], acc);
-            acc = fma(wp1[2], q[r][R + 1], acc);
-            if constexpr (R == 2) acc = fma(wp2[2], q[r][R + 2], acc);
-            const double Lv = acc;  // the right-hand side at this point
+            // partial sums per axis keep the dependent FMA chains short
+            double ax = wm1[0] * yrow[-1];
+            ax = fma(wp1[0], yrow[1], ax);
+            double ay = wm1[1] * col[r + R - 1];
+            ay = fma(wp1[1], col[r + R + 1], ay);
+            double az = wm1[2] * q[r][R - 1];
+            az = fma(wp1[2], q[r][R + 1], az);
+            if constexpr (R == 2) {
+                ax = fma(wm2[0], yrow[-2], ax);
+                ax = fma(wp2[0], yrow[2], ax);
+                ay = fma(wm2[1], col[r + R - 2], ay);
+                ay = fma(wp2[1], col[r + R + 2], ay);
+                az = fma(wm2[2], q[r][R - 2], az);
+                az = fma(wp2[2], q[r][R + 2], az);
+            }
+            const double Lv = fma(w0, yc, ax) + (ay + az);  // right-hand side at this point
 
             if (col_ok && row < h) {
                 const size_t g = (size_t(z) * n + (y0 + row)) * n + x0 + tx;
@@ -304,25 +302,13 @@ stencil_kernel(const StencilArgs a) {
                 }
             }
         }
-        (void)NP;
         // shift the z queue
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
 #pragma unroll
             for (int o = 0; o < Q - 1; ++o) q[r][o] = q[r][o + 1];
-
-        __syncthreads();  // every read of element i + R (and earlier) is done
-        if (warp == 0) {
-            bool fenced = false;
-            while (e_next < E && e_next - DEPTH <= i + R) {
-                if (!fenced) { fence_proxy_async(); fenced = true; }
-                issue_element<KIND>(a, ring, bars, e_next, z_begin, nz, x0, w, y0, h, lane);
-                ++e_next;
-            }
-        } else {
-            while (e_next < E && e_next - DEPTH <= i + R) ++e_next;
-        }
     }
+    cp_async_wait<0>();
 }
 
 // Advance the nu-table cursor after a batch of steps (last node of a graph).

@@ -64,7 +64,8 @@ static pr_status fail(pr_status s, const char *fmt, ...) {
 namespace {
 
 struct LaunchCfg {
-    int tiles_x = 0, tiles_y = 0, cz = 0, chunks_z = 0, blocks = 0, occ = 0;
+    int tiles_x = 0, tiles_y = 0, cz = 0, chunks_z = 0, blocks = 0, occ = 0, threads = 0;
+    size_t smem = 0;
 };
 
 struct NuTable {
@@ -82,6 +83,7 @@ constexpr int COARSE_PAIRS = 16;  // Euler step pairs per CUDA graph (32 kernels
 
 struct pr_grid {
     int dev = 0;
+    int variant = 0;                    // stencil tile variant (PR_TILE env, tuning)
     pr_problem prob{};
     int n = 0;
     int64_t N = 0;
@@ -113,19 +115,22 @@ struct pr_grid {
     double timings[5] = {0, 0, 0, 0, 0};
 };
 
-template <int KIND>
-static pr_status setup_kind(pr_grid *g) {
-    const size_t smem = Layout<KIND>::SMEM_BYTES;
-    CK(cudaFuncSetAttribute(stencil_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <int KIND, class C>
+static pr_status setup_kind_cfg(pr_grid *g) {
+    const size_t smem = Layout<KIND, C>::SMEM_BYTES;
+    CK(cudaFuncSetAttribute(stencil_kernel<KIND, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(smem)));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil_kernel<KIND>, NTHREADS, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil_kernel<KIND, C>, C::NTHREADS,
+                                                     smem));
     if (occ < 1) return fail(PR_ECUDA, "stencil kernel %d cannot be resident", KIND);
     LaunchCfg &c = g->lc[KIND];
     const int n = g->n;
     c.occ = occ;
+    c.threads = C::NTHREADS;
+    c.smem = smem;
     c.tiles_x = (n + TX - 1) / TX;
-    c.tiles_y = (n + TY - 1) / TY;
+    c.tiles_y = (n + C::TY - 1) / C::TY;
     const int tiles = c.tiles_x * c.tiles_y;
     const int slots = g->sms * occ;
     const int R = Traits<KIND>::R;
@@ -154,6 +159,16 @@ static pr_status setup_kind(pr_grid *g) {
     return PR_OK;
 }
 
+template <int KIND>
+static pr_status setup_kind(pr_grid *g) {
+    switch (g->variant) {
+    case 1: return setup_kind_cfg<KIND, Tile1>(g);
+    case 2: return setup_kind_cfg<KIND, Tile2>(g);
+    case 3: return setup_kind_cfg<KIND, Tile3>(g);
+    default: return setup_kind_cfg<KIND, Tile0>(g);
+    }
+}
+
 static StencilArgs base_args(const pr_grid *g, int kind) {
     StencilArgs a{};
     const LaunchCfg &c = g->lc[kind];
@@ -175,7 +190,12 @@ static void launch_stencil(pr_grid *g, const StencilArgs &a0, cudaStream_t st) {
     a.tiles_y = c.tiles_y;
     a.cz = c.cz;
     a.chunks_z = c.chunks_z;
-    stencil_kernel<KIND><<<c.blocks, NTHREADS, Layout<KIND>::SMEM_BYTES, st>>>(a);
+    switch (g->variant) {
+    case 1: stencil_kernel<KIND, Tile1><<<c.blocks, c.threads, c.smem, st>>>(a); break;
+    case 2: stencil_kernel<KIND, Tile2><<<c.blocks, c.threads, c.smem, st>>>(a); break;
+    case 3: stencil_kernel<KIND, Tile3><<<c.blocks, c.threads, c.smem, st>>>(a); break;
+    default: stencil_kernel<KIND, Tile0><<<c.blocks, c.threads, c.smem, st>>>(a); break;
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
@@ -491,6 +511,7 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
     g->N = int64_t(n) * n * n;
     g->bytes = size_t(g->N) * sizeof(double);
     g->sms = prop.multiProcessorCount;
+    if (const char *tv = getenv("PR_TILE")) g->variant = std::max(0, std::min(3, atoi(tv)));
     auto bail = [&](pr_status s) { pr_destroy_grid(g); return s; };
 #define GK(call)                                                                            \
     do {                                                                                    \
