@@ -99,57 +99,67 @@ __device__ __forceinline__ int wrapi(int i, int n) {
     return i < 0 ? i + n : i;
 }
 
-// Issue the 16-byte copies of stream element e (plane z_begin - R + e) into
-// its ring slot: every thread takes every NTHREADS-th chunk.  Periodic wrap is
-// applied per chunk (n even => a chunk never straddles the wrap).
-template <int KIND, class C>
-__device__ __forceinline__ void issue_element(const StencilArgs &a, double *ring, int e,
-                                              int z_begin, int nz, int x0, int w, int y0,
-                                              int h) {
+// Per-thread copy plan: which 16-byte chunks of a ring slot this thread
+// fetches, as (source offset inside a z plane, destination offset inside the
+// slot).  Computed once per CTA (periodic wrap in x and y folded in), so
+// issuing a plane costs a few instructions per chunk.  n even => a chunk never
+// straddles the periodic wrap.
+template <int KIND, class C> struct CopyPlan {
     using L = Layout<KIND, C>;
-    constexpr int R = L::R, NP = L::NP;
-    const int n = a.n;
-    double *ys = ring + size_t(e % C::DEPTH) * L::SLOT_ELEMS;
-    const int z = wrapi(z_begin - R + e, n);
-    const bool pw = NP > 0 && e >= R && e < nz + R;
-    const size_t plane = size_t(z) * n * n;
-    if (w == TX && h == C::TY) {  // full tile: compile-time chunk decomposition
-        constexpr int CW = SX / 2;
-        for (int c = threadIdx.x; c < L::Y_CHUNKS; c += C::NTHREADS) {
-            const int r = c / CW, cc = c % CW;
-            int yy = y0 - R + r;
-            yy += (yy < 0) ? n : 0;
-            yy -= (yy >= n) ? n : 0;
-            int xs = x0 - HX + 2 * cc;
-            xs += (xs < 0) ? n : 0;
-            xs -= (xs >= n) ? n : 0;
-            cp_async16(ys + r * SX + 2 * cc, a.y + plane + size_t(yy) * n + xs);
-        }
-        if (pw) {
-            constexpr int PC = C::TY * (TX / 2);
-            for (int c = threadIdx.x; c < L::P_CHUNKS; c += C::NTHREADS) {
-                const int f = c / PC, rem = c % PC, r = rem / (TX / 2), cc = rem % (TX / 2);
-                const double *src = (f == 0 ? a.p0 : a.p1) + plane + size_t(y0 + r) * n + x0 + 2 * cc;
-                cp_async16(ys + L::Y_ELEMS + f * L::P_ELEMS + r * TX + 2 * cc, src);
+    static constexpr int NCY = (L::Y_CHUNKS + C::NTHREADS - 1) / C::NTHREADS;
+    static constexpr int NCP = (L::P_CHUNKS + C::NTHREADS - 1) / C::NTHREADS;
+    int ysrc[NCY], ydst[NCY];
+    int psrc[NCP > 0 ? NCP : 1], pdst[NCP > 0 ? NCP : 1];
+
+    __device__ __forceinline__ void init(int n, int x0, int w, int y0, int h) {
+        constexpr int R = L::R;
+        const int cw = (w + 2 * HX) / 2, ych = (h + 2 * R) * cw;
+#pragma unroll
+        for (int k = 0; k < NCY; ++k) {
+            const int c = threadIdx.x + k * C::NTHREADS;
+            ysrc[k] = -1;
+            ydst[k] = 0;
+            if (c < ych) {
+                const int r = c / cw, cc = c % cw;
+                ysrc[k] = wrapi(y0 - R + r, n) * n + wrapi(x0 - HX + 2 * cc, n);
+                ydst[k] = r * SX + 2 * cc;
             }
         }
-    } else {  // ragged or wrapped tile (n not a multiple of the tile, or n < TX)
-        const int cw = (w + 2 * HX) / 2, yrows = h + 2 * R;
-        for (int c = threadIdx.x; c < yrows * cw; c += C::NTHREADS) {
-            const int r = c / cw, cc = c % cw;
-            const int yy = wrapi(y0 - R + r, n), xs = wrapi(x0 - HX + 2 * cc, n);
-            cp_async16(ys + r * SX + 2 * cc, a.y + plane + size_t(yy) * n + xs);
-        }
-        if (pw) {
-            const int pcw = w / 2, pc = h * pcw;
-            for (int c = threadIdx.x; c < NP * pc; c += C::NTHREADS) {
-                const int f = c / pc, rem = c % pc, r = rem / pcw, cc = rem % pcw;
-                const double *src = (f == 0 ? a.p0 : a.p1) + plane + size_t(y0 + r) * n + x0 + 2 * cc;
-                cp_async16(ys + L::Y_ELEMS + f * L::P_ELEMS + r * TX + 2 * cc, src);
+        if constexpr (NCP > 0) {
+            const int pcw = w / 2, pch = h * pcw;
+#pragma unroll
+            for (int k = 0; k < NCP; ++k) {
+                const int c = threadIdx.x + k * C::NTHREADS;
+                psrc[k] = -1;
+                pdst[k] = 0;
+                if (c < L::NP * pch) {
+                    const int f = c / pch, rem = c % pch, r = rem / pcw, cc = rem % pcw;
+                    // field 1 chunks are marked by the offset bias (1 << 30)
+                    psrc[k] = (f << 30) | ((y0 + r) * n + x0 + 2 * cc);
+                    pdst[k] = L::Y_ELEMS + f * L::P_ELEMS + r * TX + 2 * cc;
+                }
             }
         }
     }
-}
+
+    __device__ __forceinline__ void issue(const StencilArgs &a, double *slot, size_t plane,
+                                          bool pw) const {
+#pragma unroll
+        for (int k = 0; k < NCY; ++k)
+            if (ysrc[k] >= 0) cp_async16(slot + ydst[k], a.y + plane + ysrc[k]);
+        if constexpr (NCP > 0) {
+            if (pw) {
+#pragma unroll
+                for (int k = 0; k < NCP; ++k) {
+                    if (psrc[k] >= 0) {
+                        const double *base = (psrc[k] >> 30) ? a.p1 : a.p0;
+                        cp_async16(slot + pdst[k], base + plane + (psrc[k] & ((1 << 30) - 1)));
+                    }
+                }
+            }
+        }
+    }
+};
 
 // One fused stencil pass.  Stream elements e = 0 .. nz+2R-1 are the planes
 // z_begin-R .. z_begin+nz+R-1 (periodic in z); the pointwise planes ride along
@@ -173,14 +183,20 @@ stencil_kernel(const StencilArgs a) {
     const int z_begin = cz * a.cz;
     const int nz = min(a.cz, n - z_begin);
     const int E = nz + 2 * R;
+    const size_t nn = size_t(n) * n;
 
     const int tx = threadIdx.x % TX;
     const int ty = threadIdx.x / TX;
     const int row0 = ty * RPT;  // first tile row of this thread
 
+    CopyPlan<KIND, C> plan;
+    plan.init(n, x0, w, y0, h);
+    auto plane_of = [&](int e) { return size_t(wrapi(z_begin - R + e, n)) * nn; };
+
     // prologue: DEPTH elements in flight, one commit group each
+#pragma unroll 1
     for (int e = 0; e < DEPTH; ++e) {
-        if (e < E) issue_element<KIND, C>(a, ring, e, z_begin, nz, x0, w, y0, h);
+        if (e < E) plan.issue(a, ring + size_t(e) * L::SLOT_ELEMS, plane_of(e), e >= R && e < nz + R);
         cp_async_commit();
     }
     int e_next = DEPTH;
@@ -218,6 +234,14 @@ stencil_kernel(const StencilArgs a) {
     }
     const double dt = a.dt;
     const bool col_ok = tx < w;
+    const int rows_ok = h - row0;  // rows r < rows_ok of this thread are inside the tile
+
+    // per-thread offsets inside a slot and inside a plane
+    const int s_off = (R + row0) * SX + HX + tx;     // centre of the first row, stencil plane
+    const int p_off = L::Y_ELEMS + row0 * TX + tx;   // first row, pointwise plane 0
+    double *o0 = a.o0 + size_t(z_begin) * nn + size_t(y0 + row0) * n + x0 + tx;
+    double *o1 = (KIND == K_S1 || KIND == K_S2 || KIND == K_S3) ?
+                 a.o1 + size_t(z_begin) * nn + size_t(y0 + row0) * n + x0 + tx : nullptr;
 
     double q[RPT][Q];  // z queue: q[r][R + o] = Y(z + o) at (x, row0 + r)
     // initial queue fill from elements 0 .. 2R-1
@@ -225,11 +249,14 @@ stencil_kernel(const StencilArgs a) {
     __syncthreads();
 #pragma unroll
     for (int e = 0; e < 2 * R; ++e) {
-        const double *ys = ring + size_t(e % DEPTH) * L::SLOT_ELEMS;
+        const double *ys = ring + size_t(e) * L::SLOT_ELEMS + s_off;
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) q[r][e] = ys[(R + row0 + r) * SX + HX + tx];
+        for (int r = 0; r < RPT; ++r) q[r][e] = ys[r * SX];
     }
+    int slot_c = R, slot_q = 2 * R;      // ring slots of elements i+R and i+2R
+    int slot_issue = e_next % DEPTH;     // slot of element e_next
 
+#pragma unroll 1
     for (int i = 0; i < nz; ++i) {
         // own copies of element i+2R have landed ...
         if (i + R + 1 >= DEPTH) cp_async_wait<DEPTH - R - 2>();
@@ -237,32 +264,32 @@ stencil_kernel(const StencilArgs a) {
         // ... and everyone's; every read of element i-1+R (and older) is done
         __syncthreads();
         while (e_next < E && e_next - DEPTH <= i - 1 + R) {
-            issue_element<KIND, C>(a, ring, e_next, z_begin, nz, x0, w, y0, h);
+            plan.issue(a, ring + size_t(slot_issue) * L::SLOT_ELEMS, plane_of(e_next),
+                       e_next >= R && e_next < nz + R);
             ++e_next;
+            slot_issue = (slot_issue + 1 == DEPTH) ? 0 : slot_issue + 1;
         }
         cp_async_commit();
 
         {
-            const double *ys = ring + size_t((i + 2 * R) % DEPTH) * L::SLOT_ELEMS;
+            const double *yq = ring + size_t(slot_q) * L::SLOT_ELEMS + s_off;
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) q[r][2 * R] = ys[(R + row0 + r) * SX + HX + tx];
+            for (int r = 0; r < RPT; ++r) q[r][2 * R] = yq[r * SX];
         }
-        const double *ys = ring + size_t((i + R) % DEPTH) * L::SLOT_ELEMS;
-        const double *ps = ys + L::Y_ELEMS;
-        const int z = z_begin + i;
+        const double *ys = ring + size_t(slot_c) * L::SLOT_ELEMS + s_off;
+        const double *ps = ring + size_t(slot_c) * L::SLOT_ELEMS + p_off;
 
         // y column above/below the RPT rows (centres come from the queue)
         double col[RPT + 2 * R];
 #pragma unroll
         for (int r = 0; r < RPT + 2 * R; ++r) {
             if (r >= R && r < R + RPT) col[r] = q[r - R][R];
-            else col[r] = ys[(row0 + r) * SX + HX + tx];
+            else col[r] = ys[(r - R) * SX];
         }
 
 #pragma unroll
         for (int r = 0; r < RPT; ++r) {
-            const int row = row0 + r;
-            const double *yrow = ys + (R + row) * SX + HX + tx;
+            const double *yrow = ys + r * SX;
             const double yc = q[r][R];
             // partial sums per axis keep the dependent FMA chains short
             double ax = wm1[0] * yrow[-1];
@@ -281,32 +308,36 @@ stencil_kernel(const StencilArgs a) {
             }
             const double Lv = fma(w0, yc, ax) + (ay + az);  // right-hand side at this point
 
-            if (col_ok && row < h) {
-                const size_t g = (size_t(z) * n + (y0 + row)) * n + x0 + tx;
+            if (col_ok && r < rows_ok) {
+                const size_t g = size_t(r) * n;
                 if (KIND == K_COARSE) {
-                    a.o0[g] = yc + dt * Lv;
+                    o0[g] = yc + dt * Lv;
                 } else if (KIND == K_S1) {                        // y = u
-                    a.o0[g] = yc + (dt / 6.0) * Lv;               // acc = u + dt/6 k1
-                    a.o1[g] = yc + (dt / 2.0) * Lv;               // Ya  = u + dt/2 k1
+                    o0[g] = yc + (dt / 6.0) * Lv;                 // acc = u + dt/6 k1
+                    o1[g] = yc + (dt / 2.0) * Lv;                 // Ya  = u + dt/2 k1
                 } else if (KIND == K_S2) {
-                    const double u = ps[row * TX + tx], ac = ps[L::P_ELEMS + row * TX + tx];
-                    a.o0[g] = ac + (dt / 3.0) * Lv;               // acc += dt/3 k2
-                    a.o1[g] = u + (dt / 2.0) * Lv;                // Yb  = u + dt/2 k2
+                    const double u = ps[r * TX], ac = ps[L::P_ELEMS + r * TX];
+                    o0[g] = ac + (dt / 3.0) * Lv;                 // acc += dt/3 k2
+                    o1[g] = u + (dt / 2.0) * Lv;                  // Yb  = u + dt/2 k2
                 } else if (KIND == K_S3) {
-                    const double u = ps[row * TX + tx], ac = ps[L::P_ELEMS + row * TX + tx];
-                    a.o0[g] = ac + (dt / 3.0) * Lv;               // acc += dt/3 k3
-                    a.o1[g] = u + dt * Lv;                        // Ya  = u + dt k3
+                    const double u = ps[r * TX], ac = ps[L::P_ELEMS + r * TX];
+                    o0[g] = ac + (dt / 3.0) * Lv;                 // acc += dt/3 k3
+                    o1[g] = u + dt * Lv;                          // Ya  = u + dt k3
                 } else {                                          // K_S4
-                    const double ac = ps[row * TX + tx];
-                    a.o0[g] = ac + (dt / 6.0) * Lv;               // u = acc + dt/6 k4
+                    const double ac = ps[r * TX];
+                    o0[g] = ac + (dt / 6.0) * Lv;                 // u = acc + dt/6 k4
                 }
             }
         }
-        // shift the z queue
+        // shift the z queue, advance slots and output planes
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
 #pragma unroll
             for (int o = 0; o < Q - 1; ++o) q[r][o] = q[r][o + 1];
+        slot_c = (slot_c + 1 == DEPTH) ? 0 : slot_c + 1;
+        slot_q = (slot_q + 1 == DEPTH) ? 0 : slot_q + 1;
+        o0 += nn;
+        if (KIND == K_S1 || KIND == K_S2 || KIND == K_S3) o1 += nn;
     }
     cp_async_wait<0>();
 }
