@@ -1,0 +1,40 @@
+"""Multi-GPU Parareal (NCCL hand-off) — runs tools/mgpu_check.py under torchrun
+when at least 2 GPUs are visible; W-invariance is bitwise, oracle parity 1e-12."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def ngpus():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("W,n,Np,K", [(2, 32, 4, 2), (2, 32, 2, 2), (2, 40, 4, 3), (4, 32, 4, 2),
+                                      (4, 32, 8, 3), (8, 32, 8, 3), (2, 128, 2, 1)])
+def test_parareal_multi_gpu(W, n, Np, K):
+    if ngpus() < W:
+        pytest.skip(f"needs {W} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={W}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "tools", "mgpu_check.py"), str(n), str(Np), str(K)]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert res.returncode == 0 and lines, res.stdout[-3000:] + res.stderr[-3000:]
+    info = json.loads(lines[-1])
+    assert info["ok"] and info["bitwise_equal_to_1gpu"], info
