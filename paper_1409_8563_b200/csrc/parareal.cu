@@ -22,6 +22,7 @@
 
 #include "../../include/parareal.h"
 #include "kernels.cuh"
+#include "fused.cuh"
 
 using namespace prk;
 
@@ -84,6 +85,8 @@ constexpr int COARSE_PAIRS = 16;  // Euler step pairs per CUDA graph (32 kernels
 struct pr_grid {
     int dev = 0;
     int variant = 0;                    // stencil tile variant (PR_TILE env, tuning)
+    bool f2 = false;                    // fused two-kernel RK4 step (tile-aligned n)
+    LaunchCfg lf[2];                    // launch configs of fused_kernel<K_A>, <K_B>
     pr_problem prob{};
     int n = 0;
     int64_t N = 0;
@@ -169,6 +172,63 @@ static pr_status setup_kind(pr_grid *g) {
     }
 }
 
+// z-chunk count that fills whole waves of resident CTAs with little halo re-read
+static int pick_chunks(int n, int tiles, int slots, int halo) {
+    int best_chunks = 1;
+    double best = -1.0;
+    const int min_cz = std::min(n, 8);
+    for (int ch = 1; ch <= n / min_cz; ++ch) {
+        const int cz = (n + ch - 1) / ch;
+        const int che = (n + cz - 1) / cz;
+        const long items = long(tiles) * che;
+        const long waves = (items + slots - 1) / slots;
+        const double eff = double(items) / double(waves * slots);
+        const double over = 1.0 + 0.5 * double(2 * halo) / double(cz);
+        const double score = eff / over;
+        if (score > best + 1e-9) { best = score; best_chunks = che; }
+    }
+    if (const char *env = getenv("PR_CHUNKS_Z")) {
+        int v = atoi(env);
+        if (v >= 1 && v <= n) best_chunks = v;
+    }
+    return best_chunks;
+}
+
+template <int KB>
+static pr_status setup_fused(pr_grid *g) {
+    using C = Fused0;
+    const size_t smem = C::template smem_bytes<KB>();
+    CK(cudaFuncSetAttribute(fused_kernel<KB, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(smem)));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel<KB, C>, C::NT, smem));
+    if (occ < 1) return fail(PR_ECUDA, "fused kernel %d cannot be resident", KB);
+    LaunchCfg &c = g->lf[KB];
+    const int n = g->n;
+    c.occ = occ;
+    c.threads = C::NT;
+    c.smem = smem;
+    c.tiles_x = n / C::TXO;
+    c.tiles_y = n / C::TYO;
+    const int ch = pick_chunks(n, c.tiles_x * c.tiles_y, g->sms * occ, 4);
+    c.cz = (n + ch - 1) / ch;
+    c.chunks_z = (n + c.cz - 1) / c.cz;
+    c.blocks = c.tiles_x * c.tiles_y * c.chunks_z;
+    return PR_OK;
+}
+
+template <int KB>
+static void launch_fused(pr_grid *g, const StencilArgs &a0, cudaStream_t st) {
+    StencilArgs a = a0;
+    const LaunchCfg &c = g->lf[KB];
+    a.tiles_x = c.tiles_x;
+    a.tiles_y = c.tiles_y;
+    a.cz = c.cz;
+    a.chunks_z = c.chunks_z;
+    fused_kernel<KB, Fused0><<<c.blocks, c.threads, c.smem, st>>>(a);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 static StencilArgs base_args(const pr_grid *g, int kind) {
     StencilArgs a{};
     const LaunchCfg &c = g->lc[kind];
@@ -219,6 +279,23 @@ static void enqueue_fine_step(pr_grid *g, const double *u_src, double *u_dst, in
     // S4: k4 = L(Ya); u = acc + dt/6 k4
     a.y = g->ya; a.p0 = g->acc; a.p1 = nullptr; a.o0 = u_dst; a.o1 = nullptr;
     launch_stencil<K_S4>(g, a, st);
+}
+
+// One classical RK4 step as two fused kernels (fused.cuh): state u_src ->
+// new state in acc_dst (u_src is only read; Yb lives in g->ya).
+static void enqueue_fine_step2(pr_grid *g, const double *u_src, double *acc_dst, int j_local,
+                               double dt, cudaStream_t st) {
+    StencilArgs a = base_args(g, K_S1);
+    a.nu_tab = g->tab_f.d;
+    a.nu_pos = g->d_pos + 0;
+    a.j_local = j_local;
+    a.dt = dt;
+    // K_A: k1 = L(u), Ya (shared), k2 = L(Ya); acc = u + dt/6 k1 + dt/3 k2; Yb = u + dt/2 k2
+    a.y = u_src; a.p0 = nullptr; a.p1 = nullptr; a.o0 = acc_dst; a.o1 = g->ya;
+    launch_fused<K_A>(g, a, st);
+    // K_B: k3 = L(Yb), Ya' = u + dt k3 (shared), k4 = L(Ya'); u_new = acc + dt/3 k3 + dt/6 k4
+    a.y = g->ya; a.p0 = u_src; a.p1 = acc_dst; a.o0 = acc_dst; a.o1 = nullptr;
+    launch_fused<K_B>(g, a, st);
 }
 
 // One forward-Euler step (Alg.2).
@@ -325,6 +402,12 @@ static pr_status get_graph(pr_grid *g, int kind, double *u, double dt, cudaGraph
     if (kind == 0) {
         for (int b = 0; b < FINE_BATCH; ++b) enqueue_fine_step(g, u, u, b, dt, g->cap_stream);
         advance_pos_kernel<<<1, 1, 0, g->cap_stream>>>(g->d_pos + 0, FINE_BATCH);
+    } else if (kind == 2) {  // fused path: state ping-pongs u -> acc -> u
+        for (int b = 0; b < FINE_BATCH; b += 2) {
+            enqueue_fine_step2(g, u, g->acc, b, dt, g->cap_stream);
+            enqueue_fine_step2(g, g->acc, u, b + 1, dt, g->cap_stream);
+        }
+        advance_pos_kernel<<<1, 1, 0, g->cap_stream>>>(g->d_pos + 0, FINE_BATCH);
     } else {
         for (int b = 0; b < COARSE_PAIRS; ++b) {
             enqueue_coarse_step(g, u, g->ctmp, 2 * b, dt, g->cap_stream);
@@ -350,6 +433,51 @@ static pr_status get_graph(pr_grid *g, int kind, double *u, double dt, cudaGraph
     return PR_OK;
 }
 
+// Fused path: the state ping-pongs between u_out and g->acc; the step parity
+// is arranged so the last step lands in u_out.
+static pr_status run_fine2(pr_grid *g, const double *uin, double *uout, int64_t nsteps,
+                           long long base, double dt, cudaStream_t st) {
+    int64_t done = 0;
+    int jl = 0;
+    const double *state = uout;
+    if (uin != uout) {
+        double *dst = (nsteps % 2) ? uout : g->acc;
+        enqueue_fine_step2(g, uin, dst, jl++, dt, st);
+        state = dst;
+        done = 1;
+        if (state == g->acc) {
+            enqueue_fine_step2(g, g->acc, uout, jl++, dt, st);
+            state = uout;
+            done = 2;
+        }
+        CKL();
+        CKS(set_pos(g, 0, base + done, st));
+        jl = 0;
+    }
+    if (nsteps - done >= FINE_BATCH) {
+        cudaGraphExec_t ge;
+        CKS(get_graph(g, 2, uout, dt, &ge));
+        while (nsteps - done >= FINE_BATCH) {
+            CK(cudaGraphLaunch(ge, st));
+            g_launches.fetch_add(2 * FINE_BATCH + 1, std::memory_order_relaxed);
+            done += FINE_BATCH;
+        }
+    }
+    while (nsteps - done >= 2) {
+        enqueue_fine_step2(g, uout, g->acc, jl++, dt, st);
+        enqueue_fine_step2(g, g->acc, uout, jl++, dt, st);
+        done += 2;
+    }
+    if (done < nsteps) {  // in place with an odd count: last step into acc, copy back
+        enqueue_fine_step2(g, uout, g->acc, jl++, dt, st);
+        CK(cudaMemcpyAsync(uout, g->acc, g->bytes, cudaMemcpyDeviceToDevice, st));
+        ++done;
+    }
+    (void)state;
+    CKL();
+    return PR_OK;
+}
+
 static pr_status run_fine(pr_grid *g, const double *uin, double *uout, int64_t step0,
                           int64_t nsteps, double dt, cudaStream_t st) {
     if (nsteps == 0) {
@@ -357,6 +485,11 @@ static pr_status run_fine(pr_grid *g, const double *uin, double *uout, int64_t s
         return PR_OK;
     }
     CKS(ensure_table(g, 1, dt, step0, step0 + nsteps, st));
+    if (g->f2) {
+        const long long b0 = step0 - g->tab_f.lo;
+        CKS(set_pos(g, 0, b0, st));
+        return run_fine2(g, uin, uout, nsteps, b0, dt, st);
+    }
     const long long base = step0 - g->tab_f.lo;
     int64_t done = 0;
     CKS(set_pos(g, 0, base, st));
@@ -541,6 +674,14 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
     if ((s = setup_kind<K_S2>(g)) != PR_OK) return bail(s);
     if ((s = setup_kind<K_S3>(g)) != PR_OK) return bail(s);
     if ((s = setup_kind<K_S4>(g)) != PR_OK) return bail(s);
+    {
+        const char *fe = getenv("PR_F2");
+        g->f2 = (n % Fused0::TXO == 0) && (n % Fused0::TYO == 0) && !(fe && fe[0] == '0');
+    }
+    if (g->f2) {
+        if ((s = setup_fused<K_A>(g)) != PR_OK) return bail(s);
+        if ((s = setup_fused<K_B>(g)) != PR_OK) return bail(s);
+    }
     if ((s = ensure_red(g, 8)) != PR_OK) return bail(s);
     // generous initial table capacities (graphs capture the pointers)
     GK(cudaMalloc(&g->tab_f.d, (size_t(1) << 20) * sizeof(double)));

@@ -42,7 +42,7 @@ def oproblem(n, c=PARITY_C, nu0=0.1, omega=100.0, T=0.1, nu_mode=0):
     return oracle.Problem(n, c=c, nu0=nu0, omega=omega, T=T, nu_mode=nu_mode)
 
 
-@pytest.mark.parametrize("n", [4, 8, 12, 32, 40, 48, 64])
+@pytest.mark.parametrize("n", [4, 8, 12, 32, 40, 48, 64, 96])
 @pytest.mark.parametrize("nu_mode", [0, 1])
 def test_fine_steps(n, nu_mode):
     u0 = random_field(n, 0)
@@ -214,6 +214,26 @@ def test_parareal_small_random_vs_oracle():
 
 
 # ---------------------------------------------------------- full BASELINE sizes
+@pytest.mark.parametrize("f2", ["1", "0"])
+@pytest.mark.parametrize("n", [32, 64])
+def test_fine_paths_agree(n, f2, monkeypatch):
+    """Both F implementations (fused two-kernel step for tile-aligned n, four
+    stage passes otherwise) against the oracle, odd/even step counts, in place."""
+    monkeypatch.setenv("PR_F2", f2)
+    g = pr.Grid(pr.Problem(n, c=PARITY_C))
+    u0 = random_field(n, 30)
+    p = oproblem(n)
+    dt = 2e-4 * (32 / n) ** 2
+    for step0, steps in ((0, 1), (3, 2), (5, 17), (2, 33), (1, 16)):
+        out = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+        pr.pr_fine(g, dev(u0), out, step0, steps, dt)
+        assert rel(out, oracle.fine(p, u0, step0, steps, dt)) <= TOL, (step0, steps)
+        u = dev(u0)
+        pr.pr_fine(g, u, u, step0, steps, dt)
+        assert torch.equal(u, out)
+    g.destroy()
+
+
 @pytest.mark.parametrize("n", [128, 256])
 def test_full_size_steps_vs_oracle(n):
     """Launch configuration bench.py times, a few steps, all n^3 outputs."""

@@ -11,13 +11,15 @@ import torch  # noqa: E402
 import paper_1409_8563_b200 as pr  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
-variants = [int(v) for v in sys.argv[2:]] or [0, 1, 2, 3]
+variants = [v for v in sys.argv[2:]] or ["0", "1", "2", "3"]
 chunks = os.environ.get("BENCH_CHUNKS", "").split(",") if os.environ.get("BENCH_CHUNKS") else [None]
 ref = None
 u0 = None
 for ch in chunks:
     for v in variants:
-        os.environ["PR_TILE"] = str(v)
+        # "f2" = fused two-kernel RK4 step; "0".."3" = four-stage tile variants
+        os.environ["PR_F2"] = "1" if v == "f2" else "0"
+        os.environ["PR_TILE"] = "0" if v == "f2" else str(v)
         if ch is None:
             os.environ.pop("PR_CHUNKS_Z", None)
         else:
