@@ -25,8 +25,8 @@ namespace prk {
 
 enum Kind2 { K_A = 0, K_B = 1 };
 
-template <int TYO_, int DEPTH_> struct FusedCfg {
-    static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, RPT = 4;
+template <int TYO_, int DEPTH_, int MINB_ = 1> struct FusedCfg {
+    static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, RPT = 4, MINB = MINB_;
     static constexpr int EW = TXO + 4, EH = TYO + 4;   // stage-A (extended) region
     static constexpr int IW = TXO + 8, IH = TYO + 8;   // input region
     static constexpr int A_ITEMS = EW * (EH / RPT);
@@ -44,10 +44,12 @@ template <int TYO_, int DEPTH_> struct FusedCfg {
         return sizeof(double) * (size_t(DEPTH) * Y_ELEMS + 3 * Z_ELEMS + 3 * NTV<KB> * T_ELEMS);
     }
 };
-using Fused0 = FusedCfg<16, 6>;
+using Fused0 = FusedCfg<16, 6, 1>;
+using Fused1 = FusedCfg<16, 6, 2>;   // register-capped for 2 CTAs/SM
+using Fused2 = FusedCfg<8, 6, 2>;    // smaller tile
 
 template <int KB, class C>
-__global__ void __launch_bounds__(C::NT)
+__global__ void __launch_bounds__(C::NT, C::MINB)
 fused_kernel(const StencilArgs a) {
     constexpr int RPT = C::RPT, DEPTH = C::DEPTH, EW = C::EW, IW = C::IW, TXO = C::TXO;
     constexpr int NTV = C::template NTV<KB>;

@@ -86,6 +86,7 @@ struct pr_grid {
     int dev = 0;
     int variant = 0;                    // stencil tile variant (PR_TILE env, tuning)
     bool f2 = false;                    // fused two-kernel RK4 step (tile-aligned n)
+    int fvariant = 0;                   // fused tile variant (PR_FTILE env, tuning)
     LaunchCfg lf[2];                    // launch configs of fused_kernel<K_A>, <K_B>
     pr_problem prob{};
     int n = 0;
@@ -194,9 +195,8 @@ static int pick_chunks(int n, int tiles, int slots, int halo) {
     return best_chunks;
 }
 
-template <int KB>
-static pr_status setup_fused(pr_grid *g) {
-    using C = Fused0;
+template <int KB, class C>
+static pr_status setup_fused_cfg(pr_grid *g) {
     const size_t smem = C::template smem_bytes<KB>();
     CK(cudaFuncSetAttribute(fused_kernel<KB, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(smem)));
@@ -218,6 +218,15 @@ static pr_status setup_fused(pr_grid *g) {
 }
 
 template <int KB>
+static pr_status setup_fused(pr_grid *g) {
+    switch (g->fvariant) {
+    case 1: return setup_fused_cfg<KB, Fused1>(g);
+    case 2: return setup_fused_cfg<KB, Fused2>(g);
+    default: return setup_fused_cfg<KB, Fused0>(g);
+    }
+}
+
+template <int KB>
 static void launch_fused(pr_grid *g, const StencilArgs &a0, cudaStream_t st) {
     StencilArgs a = a0;
     const LaunchCfg &c = g->lf[KB];
@@ -225,7 +234,11 @@ static void launch_fused(pr_grid *g, const StencilArgs &a0, cudaStream_t st) {
     a.tiles_y = c.tiles_y;
     a.cz = c.cz;
     a.chunks_z = c.chunks_z;
-    fused_kernel<KB, Fused0><<<c.blocks, c.threads, c.smem, st>>>(a);
+    switch (g->fvariant) {
+    case 1: fused_kernel<KB, Fused1><<<c.blocks, c.threads, c.smem, st>>>(a); break;
+    case 2: fused_kernel<KB, Fused2><<<c.blocks, c.threads, c.smem, st>>>(a); break;
+    default: fused_kernel<KB, Fused0><<<c.blocks, c.threads, c.smem, st>>>(a); break;
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
@@ -676,6 +689,7 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
     if ((s = setup_kind<K_S4>(g)) != PR_OK) return bail(s);
     {
         const char *fe = getenv("PR_F2");
+        if (const char *fv = getenv("PR_FTILE")) g->fvariant = std::max(0, std::min(2, atoi(fv)));
         g->f2 = (n % Fused0::TXO == 0) && (n % Fused0::TYO == 0) && !(fe && fe[0] == '0');
     }
     if (g->f2) {

@@ -18,8 +18,9 @@ u0 = None
 for ch in chunks:
     for v in variants:
         # "f2" = fused two-kernel RK4 step; "0".."3" = four-stage tile variants
-        os.environ["PR_F2"] = "1" if v == "f2" else "0"
-        os.environ["PR_TILE"] = "0" if v == "f2" else str(v)
+        os.environ["PR_F2"] = "1" if v.startswith("f2") else "0"
+        os.environ["PR_FTILE"] = v[3:] if v.startswith("f2_") else "0"
+        os.environ["PR_TILE"] = "0" if v.startswith("f2") else str(v)
         if ch is None:
             os.environ.pop("PR_CHUNKS_Z", None)
         else:
