@@ -9,15 +9,22 @@
 //                       k4 = L(Ya') on the tile;
 //                       u_new = acc + dt/3 k3 + dt/6 k4  (written over acc).
 //                       HBM: read Yb, u, acc, write u_new        (32 B/point)
-// One RK4 step moves 56 B/point instead of 128 B/point for four stage passes.
+// One RK4 step moves 56 B/point instead of 128 B/point for four stage passes,
+// with exactly the same floating-point operation sequence per point as the
+// four-stage kernels (the two paths agree bitwise).
 //
-// Geometry: output tile TXO x TYO (x, y); stage A runs on the extended region
-// (TXO+4) x (TYO+4); its input is read on (TXO+8) x (TYO+8).  A CTA marches a
-// z chunk; stage A lags the input stream by 2 planes and stage B lags stage A
-// by 2 planes.  The stencil input is streamed into a DEPTH-slot shared ring
-// with 16-byte cp.async copies (periodic wrap folded into a per-thread plan),
-// Ya lives in a 3-plane shared ring, z neighbours in per-thread register
-// queues, each thread handles RPT = 4 consecutive rows (shared y neighbours).
+// Geometry: output tile 32 x TYO (x, y); stage A runs on the extended region
+// 36 x (TYO+4); its input is read on 40 x (TYO+8).  A CTA marches a z chunk.
+// Warp specialisation:
+//   * stage-A warps stream the input planes into a DEPTH-slot shared ring with
+//     16-byte cp.async copies (periodic wrap folded into a per-thread copy plan,
+//     synchronised among themselves by a named barrier), keep z neighbours in
+//     register queues (RPT = 4 consecutive rows per thread), and write each
+//     intermediate plane (Ya or Ya') plus the per-tile-point data stage B needs
+//     into a ZD-slot shared ring;
+//   * stage-B warps consume that ring (mbarrier full/empty hand-off, so both
+//     stages run concurrently, stage A up to ZD-2 planes ahead) and store the
+//     outputs to HBM coalesced along x.
 #pragma once
 #include "kernels.cuh"
 
@@ -25,56 +32,115 @@ namespace prk {
 
 enum Kind2 { K_A = 0, K_B = 1 };
 
-template <int TYO_, int DEPTH_, int MINB_ = 1> struct FusedCfg {
-    static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, RPT = 4, MINB = MINB_;
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+template <int TYO_, int DEPTH_, int ZD_, int MINB_> struct FusedCfg {
+    static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, RPT = 4, MINB = MINB_;
     static constexpr int EW = TXO + 4, EH = TYO + 4;   // stage-A (extended) region
     static constexpr int IW = TXO + 8, IH = TYO + 8;   // input region
-    static constexpr int A_ITEMS = EW * (EH / RPT);
-    static constexpr int B_ITEMS = TXO * (TYO / RPT);
-    static constexpr int NT = ((A_ITEMS + 31) / 32) * 32;
+    static constexpr int GA = EH / RPT, GB = TYO / RPT;  // row groups
+    static constexpr int EDGE_ITEMS = 4 * GA;            // ext columns 32..35
+    static constexpr int EA = (EDGE_ITEMS + 31) / 32;
+    static constexpr int WA = GA + EA, WB = GB;
+    static constexpr int NTA = 32 * WA, NTB = 32 * WB, NT = NTA + NTB;
+    static constexpr int AD = DEPTH - 2;                 // aux ring (K_B)
     static constexpr int Y_ELEMS = IH * IW;
     static constexpr int Z_ELEMS = EH * EW;
     static constexpr int T_ELEMS = TYO * TXO;
+    static constexpr int AUX_ELEMS = Z_ELEMS + T_ELEMS;  // u on the ext region, acc on the tile
     static constexpr int Y_CHUNKS = IH * (IW / 2);
-    static constexpr int NCY = (Y_CHUNKS + NT - 1) / NT;
-    static_assert(TYO % RPT == 0 && EH % RPT == 0, "rows must split into RPT groups");
-    static_assert(DEPTH >= 6, "ring too shallow");
+    static constexpr int U_CHUNKS = EH * (EW / 2);
+    static constexpr int C_CHUNKS = TYO * (TXO / 2);
+    static constexpr int NCY = (Y_CHUNKS + NTA - 1) / NTA;
+    static constexpr int NCU = (U_CHUNKS + NTA - 1) / NTA;
+    static constexpr int NCC = (C_CHUNKS + NTA - 1) / NTA;
+    static_assert(TYO % RPT == 0, "rows must split into RPT groups");
+    static_assert(DEPTH >= 6 && ZD >= 3, "rings too shallow");
     template <int KB> static constexpr int NTV = KB == K_A ? 2 : 1;
+    template <int KB> static constexpr int ZS_ELEMS = Z_ELEMS + NTV<KB> * T_ELEMS;
     template <int KB> static constexpr size_t smem_bytes() {
-        return sizeof(double) * (size_t(DEPTH) * Y_ELEMS + 3 * Z_ELEMS + 3 * NTV<KB> * T_ELEMS);
+        return sizeof(double) * (size_t(DEPTH) * Y_ELEMS + (KB == K_B ? size_t(AD) * AUX_ELEMS : 0) +
+                                 size_t(ZD) * ZS_ELEMS<KB>);
     }
 };
-using Fused0 = FusedCfg<16, 6, 1>;
-using Fused1 = FusedCfg<16, 6, 2>;   // register-capped for 2 CTAs/SM
-using Fused2 = FusedCfg<8, 6, 2>;    // smaller tile
+using Fused0 = FusedCfg<16, 6, 4, 1>;
+using Fused1 = FusedCfg<16, 6, 5, 1>;
+using Fused2 = FusedCfg<16, 7, 4, 1>;
+
+// folded 13-point operator, C3 (same order as stencil_kernel)
+struct Weights {
+    double wm1[3], wp1[3], wm2[3], wp2[3], w0;
+    __device__ __forceinline__ void set(double nu, double inv_dx, const double *c) {
+        const double al = nu * inv_dx * inv_dx / 12.0;
+        w0 = -90.0 * al;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double be = c[d] * inv_dx / 12.0;
+            wp2[d] = -al + be; wp1[d] = 16.0 * al - 8.0 * be;
+            wm1[d] = 16.0 * al + 8.0 * be; wm2[d] = -al - be;
+        }
+    }
+    // xr: pointer to the centre in the current plane (x neighbours at +-1, +-2);
+    // ym2..yp2: y neighbours; q: z queue (q[2] = centre)
+    __device__ __forceinline__ double apply(const double *xr, double ym2, double ym1, double yp1,
+                                            double yp2, const double *q) const {
+        double ax = wm1[0] * xr[-1];
+        ax = fma(wp1[0], xr[1], ax);
+        ax = fma(wm2[0], xr[-2], ax);
+        ax = fma(wp2[0], xr[2], ax);
+        double ay = wm1[1] * ym1;
+        ay = fma(wp1[1], yp1, ay);
+        ay = fma(wm2[1], ym2, ay);
+        ay = fma(wp2[1], yp2, ay);
+        double az = wm1[2] * q[1];
+        az = fma(wp1[2], q[3], az);
+        az = fma(wm2[2], q[0], az);
+        az = fma(wp2[2], q[4], az);
+        return fma(w0, q[2], ax) + (ay + az);
+    }
+};
 
 template <int KB, class C>
-__global__ void __launch_bounds__(C::NT, C::MINB)
-fused_kernel(const StencilArgs a) {
-    constexpr int RPT = C::RPT, DEPTH = C::DEPTH, EW = C::EW, IW = C::IW, TXO = C::TXO;
-    constexpr int NTV = C::template NTV<KB>;
-    extern __shared__ __align__(128) double sm[];
-    double *yring = sm;                                  // DEPTH x input planes
-    double *zring = yring + size_t(DEPTH) * C::Y_ELEMS;  // 3 x intermediate planes
-    double *tring = zring + 3 * C::Z_ELEMS;              // 3 x NTV tile planes
-
+__device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, uint64_t *full,
+                                              uint64_t *empty, int x0, int y0, int z_begin,
+                                              int nz) {
+    constexpr int RPT = C::RPT, DEPTH = C::DEPTH, EW = C::EW, IW = C::IW, TXO = C::TXO,
+                  ZD = C::ZD, AD = C::AD;
+    constexpr int NTV = C::template NTV<KB>, ZS = C::template ZS_ELEMS<KB>;
+    double *yring = sm;
+    double *aring = yring + size_t(DEPTH) * C::Y_ELEMS;
+    double *zring = aring + (KB == K_B ? size_t(AD) * C::AUX_ELEMS : 0);
     const int n = a.n;
     const size_t nn = size_t(n) * n;
-    int b = blockIdx.x;
-    const int tix = b % a.tiles_x; b /= a.tiles_x;
-    const int tiy = b % a.tiles_y; b /= a.tiles_y;
-    const int x0 = tix * TXO, y0 = tiy * C::TYO;
-    const int z_begin = b * a.cz;
-    const int nz = min(a.cz, n - z_begin);
-    const int E = nz + 8;    // input planes z_begin-4 .. z_begin+nz+3
-    const int NJ = nz + 4;   // stage-A planes z_begin-2 .. z_begin+nz+1
-    const int t = threadIdx.x;
+    const int E = nz + 8, NJ = nz + 4;
+    const int t = threadIdx.x, warp = t / 32, lane = t % 32;
 
-    // copy plan of one input plane (periodic wrap in x and y folded in)
+    // copy plans (periodic wrap in x and y folded in), computed once
     int ysrc[C::NCY], ydst[C::NCY];
 #pragma unroll
     for (int k = 0; k < C::NCY; ++k) {
-        const int c = t + k * C::NT;
+        const int c = t + k * C::NTA;
         ysrc[k] = -1;
         ydst[k] = 0;
         if (c < C::Y_CHUNKS) {
@@ -83,12 +149,58 @@ fused_kernel(const StencilArgs a) {
             ydst[k] = r * IW + 2 * cc;
         }
     }
-    auto issue = [&](int e) {
-        const double *src = a.y + size_t(wrapi(z_begin - 4 + e, n)) * nn;
-        double *dst = yring + size_t(e % DEPTH) * C::Y_ELEMS;
+    int usrc[KB == K_B ? C::NCU : 1], udst[KB == K_B ? C::NCU : 1];
+    int csrc[KB == K_B ? C::NCC : 1], cdst[KB == K_B ? C::NCC : 1];
+    if constexpr (KB == K_B) {
 #pragma unroll
-        for (int k = 0; k < C::NCY; ++k)
-            if (ysrc[k] >= 0) cp_async16(dst + ydst[k], src + ysrc[k]);
+        for (int k = 0; k < C::NCU; ++k) {
+            const int c = t + k * C::NTA;
+            usrc[k] = -1;
+            udst[k] = 0;
+            if (c < C::U_CHUNKS) {
+                const int r = c / (EW / 2), cc = c % (EW / 2);
+                usrc[k] = wrapi(y0 - 2 + r, n) * n + wrapi(x0 - 2 + 2 * cc, n);
+                udst[k] = r * EW + 2 * cc;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < C::NCC; ++k) {
+            const int c = t + k * C::NTA;
+            csrc[k] = -1;
+            cdst[k] = 0;
+            if (c < C::C_CHUNKS) {
+                const int r = c / (TXO / 2), cc = c % (TXO / 2);
+                csrc[k] = (y0 + r) * n + x0 + 2 * cc;
+                cdst[k] = C::Z_ELEMS + r * TXO + 2 * cc;
+            }
+        }
+    }
+    // input element e = plane z_begin-4+e; aux j (K_B) = u on the ext region and
+    // acc on the tile at stage-A plane j (physical z_begin-2+j), issued with
+    // input element j+4 so both are waited for together.
+    auto issue = [&](int e) {
+        {
+            const double *src = a.y + size_t(wrapi(z_begin - 4 + e, n)) * nn;
+            double *dst = yring + size_t(e % DEPTH) * C::Y_ELEMS;
+#pragma unroll
+            for (int k = 0; k < C::NCY; ++k)
+                if (ysrc[k] >= 0) cp_async16(dst + ydst[k], src + ysrc[k]);
+        }
+        if constexpr (KB == K_B) {
+            const int j = e - 4;
+            if (j >= 0 && j < NJ) {
+                const size_t pl = size_t(wrapi(z_begin - 2 + j, n)) * nn;
+                double *dst = aring + size_t(j % AD) * C::AUX_ELEMS;
+#pragma unroll
+                for (int k = 0; k < C::NCU; ++k)
+                    if (usrc[k] >= 0) cp_async16(dst + udst[k], a.p0 + pl + usrc[k]);
+                if (j >= 2 && j < nz + 2) {
+#pragma unroll
+                    for (int k = 0; k < C::NCC; ++k)
+                        if (csrc[k] >= 0) cp_async16(dst + cdst[k], a.p1 + pl + csrc[k]);
+                }
+            }
+        }
     };
 #pragma unroll 1
     for (int e = 0; e < DEPTH; ++e) {
@@ -97,172 +209,176 @@ fused_kernel(const StencilArgs a) {
     }
     int e_next = DEPTH;
 
-    // nu of the two stages of this kernel: (1, 2) for K_A, (3, 4) for K_B
     const long long row = (*a.nu_pos + a.j_local) * 4;
-    const double nuA = a.nu_tab[row + (KB == K_A ? 0 : 2)];
-    const double nuB = a.nu_tab[row + (KB == K_A ? 1 : 3)];
-    // folded weights (C3): L = w0 y + sum_a [wp2 y+2 + wp1 y+1 + wm1 y-1 + wm2 y-2]
-    double wp2[3], wp1[3], wm1[3], wm2[3];
-    const double alA = nuA * a.inv_dx * a.inv_dx / 12.0, alB = nuB * a.inv_dx * a.inv_dx / 12.0;
-    const double w0A = -90.0 * alA, w0B = -90.0 * alB;
-    double be[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) be[d] = a.c[d] * a.inv_dx / 12.0;
-    // the advection part is the same in both stages, the diffusion part scales with nu
+    Weights W;
+    W.set(a.nu_tab[row + (KB == K_A ? 0 : 2)], a.inv_dx, a.c);
     const double dt = a.dt;
 
-    // stage-A item: column cA of the extended region, rows rA0 .. rA0+3
-    const bool actA = t < C::A_ITEMS;
-    const int cA = t % EW, rA0 = (t / EW) * RPT;
-    // stage-B item: column cB of the tile, rows rB0 .. rB0+3
-    const bool actB = t < C::B_ITEMS;
-    const int cB = t % TXO, rB0 = (t / TXO) * RPT;
-
-    // K_B: the base field u on the extended points and acc on the tile points
-    // are read from global memory one iteration ahead into registers.
-    int uoffA[RPT];
-    const int uxA = wrapi(x0 - 2 + cA, n);
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) uoffA[r] = wrapi(y0 - 2 + rA0 + r, n) * n + uxA;
-    double ubase[RPT], accp[RPT];
-    auto prefetch_u = [&](int j) {  // base for stage-A plane j (physical z_begin-2+j)
-        const double *src = a.p0 + size_t(wrapi(z_begin - 2 + j, n)) * nn;
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) ubase[r] = src[uoffA[r]];
-    };
-    auto prefetch_acc = [&](int i) {  // acc of output plane i
-        const double *src = a.p1 + size_t(z_begin + i) * nn + size_t(y0 + rB0) * n + x0 + cB;
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) accp[r] = src[size_t(r) * n];
-    };
-    if (KB == K_B) {
-        if (actA) prefetch_u(0);
+    // item: main warps own ext columns 0..31 of row group `warp`; edge warps own
+    // ext columns 32..35 of row group idx/4.
+    bool valid = true;
+    int c, g;
+    if (warp < C::GA) {
+        c = lane;
+        g = warp;
+    } else {
+        const int idx = (warp - C::GA) * 32 + lane;
+        valid = idx < C::EDGE_ITEMS;
+        c = 32 + (idx & 3);
+        g = valid ? idx >> 2 : 0;
     }
+    const int r0 = g * RPT;                  // first ext row
+    const int sY = (r0 + 2) * IW + c + 2;    // centre of the first row in an input plane
+    const int sZ = r0 * EW + c;              // same point in a Z / aux-u plane
 
-    double qa[RPT][5], qb[RPT][5];
-    // initial stage-A queue: input elements 0..3
+    double q[RPT][5];
     cp_async_wait<DEPTH - 4>();
-    __syncthreads();
-    const int sA = (rA0 + 2) * IW + cA + 2;  // centre of the first row, input plane
-    const int sB = (rB0 + 2) * EW + cB + 2;  // centre of the first row, Ya plane
-    if (actA) {
+    named_bar_sync(1, C::NTA);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const double *ys = yring + size_t(e) * C::Y_ELEMS + sA;
+    for (int e = 0; e < 4; ++e) {
+        const double *ys = yring + size_t(e) * C::Y_ELEMS + sY;
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) qa[r][e] = ys[r * IW];
-        }
+        for (int r = 0; r < RPT; ++r) q[r][e] = ys[r * IW];
     }
-    double *o0 = a.o0 + size_t(z_begin) * nn + size_t(y0 + rB0) * n + x0 + cB;
-    double *o1 = KB == K_A ? a.o1 + size_t(z_begin) * nn + size_t(y0 + rB0) * n + x0 + cB : nullptr;
 
 #pragma unroll 1
     for (int j = 0; j < NJ; ++j) {
         if (j + 4 >= DEPTH + 2) cp_async_wait<DEPTH - 4>();
         else cp_async_wait<DEPTH - 5>();
-        __syncthreads();  // input element j+4 visible; iteration j-1 finished with its slots
+        named_bar_sync(1, C::NTA);  // element j+4 (+ aux j) visible; slots of j-1 released
         while (e_next < E && e_next - DEPTH <= j + 1) issue(e_next++);
         cp_async_commit();
 
-        const int zslot = j % 3;
-        if (actA) {  // ---- stage A on the extended region, plane j
-            const double *yq = yring + size_t((j + 4) % DEPTH) * C::Y_ELEMS + sA;
+        const double *yq = yring + size_t((j + 4) % DEPTH) * C::Y_ELEMS + sY;
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) qa[r][4] = yq[r * IW];
-            const double *ys = yring + size_t((j + 2) % DEPTH) * C::Y_ELEMS + sA;
+        for (int r = 0; r < RPT; ++r) q[r][4] = yq[r * IW];
+        const double *ys = yring + size_t((j + 2) % DEPTH) * C::Y_ELEMS + sY;
+        double col[RPT + 4];
+#pragma unroll
+        for (int r = 0; r < RPT + 4; ++r)
+            col[r] = (r >= 2 && r < RPT + 2) ? q[r - 2][2] : ys[(r - 2) * IW];
+        double k[RPT];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+            k[r] = W.apply(ys + r * IW, col[r], col[r + 1], col[r + 3], col[r + 4], q[r]);
+
+        const int zslot = j % ZD;
+        if (j >= ZD) mbar_wait(&empty[zslot], ((j / ZD) & 1) ^ 1);
+        double *zs = zring + size_t(zslot) * ZS;
+        const double *au = aring + size_t(j % AD) * C::AUX_ELEMS;
+        const bool outp = j >= 2 && j < nz + 2;
+        if (valid) {
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                const double yc = q[r][2];
+                if (KB == K_A) zs[sZ + r * EW] = yc + (dt / 2.0) * k[r];            // Ya
+                else zs[sZ + r * EW] = au[sZ + r * EW] + dt * k[r];                  // Ya'
+                const int er = r0 + r;
+                if (outp && c >= 2 && c < TXO + 2 && er >= 2 && er < C::TYO + 2) {
+                    const int tp = (er - 2) * TXO + (c - 2);
+                    if (KB == K_A) {
+                        zs[C::Z_ELEMS + tp] = yc + (dt / 6.0) * k[r];               // u + dt/6 k1
+                        zs[C::Z_ELEMS + C::T_ELEMS + tp] = yc;                       // u
+                    } else {
+                        zs[C::Z_ELEMS + tp] = au[C::Z_ELEMS + tp] + (dt / 3.0) * k[r];  // acc + dt/3 k3
+                    }
+                }
+            }
+        }
+        mbar_arrive(&full[zslot]);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+#pragma unroll
+            for (int o = 0; o < 4; ++o) q[r][o] = q[r][o + 1];
+    }
+    cp_async_wait<0>();
+    (void)NTV;
+}
+
+template <int KB, class C>
+__device__ __forceinline__ void stage_b_warps(const StencilArgs &a, double *sm, uint64_t *full,
+                                              uint64_t *empty, int x0, int y0, int z_begin,
+                                              int nz) {
+    constexpr int RPT = C::RPT, EW = C::EW, TXO = C::TXO, ZD = C::ZD, DEPTH = C::DEPTH,
+                  AD = C::AD;
+    constexpr int ZS = C::template ZS_ELEMS<KB>;
+    double *zring = sm + size_t(DEPTH) * C::Y_ELEMS + (KB == K_B ? size_t(AD) * C::AUX_ELEMS : 0);
+    const int n = a.n;
+    const size_t nn = size_t(n) * n;
+    const int NJ = nz + 4;
+    const int tb = threadIdx.x - C::NTA;
+    const int c = tb % 32, g = tb / 32;
+    const int r0 = g * RPT;                       // first tile row
+    const int sZ = (r0 + 2) * EW + c + 2;         // centre of the first row in a Z plane
+    const int sT = r0 * TXO + c;
+
+    const long long row = (*a.nu_pos + a.j_local) * 4;
+    Weights W;
+    W.set(a.nu_tab[row + (KB == K_A ? 1 : 3)], a.inv_dx, a.c);
+    const double dt = a.dt;
+    double *o0 = a.o0 + size_t(z_begin) * nn + size_t(y0 + r0) * n + x0 + c;
+    double *o1 = KB == K_A ? a.o1 + size_t(z_begin) * nn + size_t(y0 + r0) * n + x0 + c : nullptr;
+
+    double q[RPT][5];
+#pragma unroll 1
+    for (int j = 0; j < NJ; ++j) {
+        const int zslot = j % ZD;
+        mbar_wait(&full[zslot], (j / ZD) & 1);
+        const double *zq = zring + size_t(zslot) * ZS + sZ;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) q[r][4] = zq[r * EW];
+        if (j >= 4) {  // output plane j-4, centred on Z plane j-2
+            const double *zs = zring + size_t((j - 2) % ZD) * ZS;
+            const double *zc = zs + sZ;
             double col[RPT + 4];
 #pragma unroll
             for (int r = 0; r < RPT + 4; ++r)
-                col[r] = (r >= 2 && r < RPT + 2) ? qa[r - 2][2] : ys[(r - 2) * IW];
-            double *zs = zring + size_t(zslot) * C::Z_ELEMS + rA0 * EW + cA;
-            const bool outp = j >= 2 && j < nz + 2;
+                col[r] = (r >= 2 && r < RPT + 2) ? q[r - 2][2] : zc[(r - 2) * EW];
 #pragma unroll
             for (int r = 0; r < RPT; ++r) {
-                const double *yr = ys + r * IW;
-                const double yc = qa[r][2];
-                double ax = (16.0 * alA + 8.0 * be[0]) * yr[-1];
-                ax = fma(16.0 * alA - 8.0 * be[0], yr[1], ax);
-                ax = fma(-alA - be[0], yr[-2], ax);
-                ax = fma(-alA + be[0], yr[2], ax);
-                double ay = (16.0 * alA + 8.0 * be[1]) * col[r + 1];
-                ay = fma(16.0 * alA - 8.0 * be[1], col[r + 3], ay);
-                ay = fma(-alA - be[1], col[r], ay);
-                ay = fma(-alA + be[1], col[r + 4], ay);
-                double az = (16.0 * alA + 8.0 * be[2]) * qa[r][1];
-                az = fma(16.0 * alA - 8.0 * be[2], qa[r][3], az);
-                az = fma(-alA - be[2], qa[r][0], az);
-                az = fma(-alA + be[2], qa[r][4], az);
-                const double kA = fma(w0A, yc, ax) + (ay + az);
-                const double base = KB == K_A ? yc : ubase[r];
-                zs[r * EW] = base + (KB == K_A ? dt / 2.0 : dt) * kA;  // Ya or Ya'
-                const int er = rA0 + r;
-                if (outp && cA >= 2 && cA < TXO + 2 && er >= 2 && er < C::TYO + 2) {
-                    double *ts = tring + size_t(zslot) * NTV * C::T_ELEMS + (er - 2) * TXO + (cA - 2);
-                    if (KB == K_A) {
-                        ts[0] = yc + (dt / 6.0) * kA;   // u + dt/6 k1
-                        ts[C::T_ELEMS] = yc;            // u
-                    } else {
-                        ts[0] = kA;                     // k3
-                    }
+                const double kB = W.apply(zc + r * EW, col[r], col[r + 1], col[r + 3], col[r + 4], q[r]);
+                const size_t gofs = size_t(r) * n;
+                if (KB == K_A) {
+                    o0[gofs] = zs[C::Z_ELEMS + sT + r * TXO] + (dt / 3.0) * kB;                 // acc
+                    o1[gofs] = zs[C::Z_ELEMS + C::T_ELEMS + sT + r * TXO] + (dt / 2.0) * kB;    // Yb
+                } else {
+                    o0[gofs] = zs[C::Z_ELEMS + sT + r * TXO] + (dt / 6.0) * kB;                 // u_new
                 }
             }
-#pragma unroll
-            for (int r = 0; r < RPT; ++r)
-#pragma unroll
-                for (int o = 0; o < 4; ++o) qa[r][o] = qa[r][o + 1];
+            o0 += nn;
+            if (KB == K_A) o1 += nn;
         }
-        if (KB == K_B && actA && j + 1 < NJ) prefetch_u(j + 1);
-        __syncthreads();  // Ya plane j visible
-        if (actB) {  // ---- stage B on the tile, output plane j-4
-            const double *zq = zring + size_t(zslot) * C::Z_ELEMS + sB;
+        if (j >= 2) mbar_arrive(&empty[(j - 2) % ZD]);
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) qb[r][4] = zq[r * EW];
-            if (j >= 4) {
-                const int i = j - 4;
-                const int cslot = (j - 2) % 3;
-                const double *zs = zring + size_t(cslot) * C::Z_ELEMS + sB;
-                const double *ts = tring + size_t(cslot) * NTV * C::T_ELEMS + rB0 * TXO + cB;
-                double col[RPT + 4];
+        for (int r = 0; r < RPT; ++r)
 #pragma unroll
-                for (int r = 0; r < RPT + 4; ++r)
-                    col[r] = (r >= 2 && r < RPT + 2) ? qb[r - 2][2] : zs[(r - 2) * EW];
-#pragma unroll
-                for (int r = 0; r < RPT; ++r) {
-                    const double *zr = zs + r * EW;
-                    const double zc = qb[r][2];
-                    double ax = (16.0 * alB + 8.0 * be[0]) * zr[-1];
-                    ax = fma(16.0 * alB - 8.0 * be[0], zr[1], ax);
-                    ax = fma(-alB - be[0], zr[-2], ax);
-                    ax = fma(-alB + be[0], zr[2], ax);
-                    double ay = (16.0 * alB + 8.0 * be[1]) * col[r + 1];
-                    ay = fma(16.0 * alB - 8.0 * be[1], col[r + 3], ay);
-                    ay = fma(-alB - be[1], col[r], ay);
-                    ay = fma(-alB + be[1], col[r + 4], ay);
-                    double az = (16.0 * alB + 8.0 * be[2]) * qb[r][1];
-                    az = fma(16.0 * alB - 8.0 * be[2], qb[r][3], az);
-                    az = fma(-alB - be[2], qb[r][0], az);
-                    az = fma(-alB + be[2], qb[r][4], az);
-                    const double kB = fma(w0B, zc, ax) + (ay + az);
-                    const size_t g = size_t(r) * n;
-                    if (KB == K_A) {
-                        o0[g] = ts[r * TXO] + (dt / 3.0) * kB;                 // acc
-                        o1[g] = ts[C::T_ELEMS + r * TXO] + (dt / 2.0) * kB;    // Yb
-                    } else {
-                        o0[g] = accp[r] + (dt / 3.0) * ts[r * TXO] + (dt / 6.0) * kB;  // u_new
-                    }
-                }
-                o0 += nn;
-                if (KB == K_A) o1 += nn;
-                (void)i;
-            }
-#pragma unroll
-            for (int r = 0; r < RPT; ++r)
-#pragma unroll
-                for (int o = 0; o < 4; ++o) qb[r][o] = qb[r][o + 1];
-            if (KB == K_B && j + 1 >= 4 && j + 1 - 4 < nz) prefetch_acc(j + 1 - 4);
-        }
+            for (int o = 0; o < 4; ++o) q[r][o] = q[r][o + 1];
     }
-    cp_async_wait<0>();
+}
+
+template <int KB, class C>
+__global__ void __launch_bounds__(C::NT, C::MINB)
+fused_kernel(const StencilArgs a) {
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) uint64_t full[C::ZD], empty[C::ZD];
+    int b = blockIdx.x;
+    const int tix = b % a.tiles_x; b /= a.tiles_x;
+    const int tiy = b % a.tiles_y; b /= a.tiles_y;
+    const int x0 = tix * C::TXO, y0 = tiy * C::TYO;
+    const int z_begin = b * a.cz;
+    const int nz = min(a.cz, a.n - z_begin);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::ZD; ++s) {
+            mbar_init(&full[s], C::NTA);
+            mbar_init(&empty[s], C::NTB);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x < C::NTA)
+        stage_a_warps<KB, C>(a, sm, full, empty, x0, y0, z_begin, nz);
+    else
+        stage_b_warps<KB, C>(a, sm, full, empty, x0, y0, z_begin, nz);
 }
 
 }  // namespace prk
