@@ -55,11 +55,12 @@ __device__ __forceinline__ void named_bar_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-template <int TYO_, int DEPTH_, int ZD_, int MINB_> struct FusedCfg {
-    static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, RPT = 4, MINB = MINB_;
+template <int TYO_, int DEPTH_, int ZD_, int MINB_, int RPTA_ = 4> struct FusedCfg {
+    static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = MINB_;
+    static constexpr int RPT = 4, RPTA = RPTA_;        // rows per thread: stage B, stage A
     static constexpr int EW = TXO + 4, EH = TYO + 4;   // stage-A (extended) region
     static constexpr int IW = TXO + 8, IH = TYO + 8;   // input region
-    static constexpr int GA = EH / RPT, GB = TYO / RPT;  // row groups
+    static constexpr int GA = EH / RPTA, GB = TYO / RPT;  // row groups
     static constexpr int EDGE_ITEMS = 4 * GA;            // ext columns 32..35
     static constexpr int EA = (EDGE_ITEMS + 31) / 32;
     static constexpr int WA = GA + EA, WB = GB;
@@ -75,7 +76,7 @@ template <int TYO_, int DEPTH_, int ZD_, int MINB_> struct FusedCfg {
     static constexpr int NCY = (Y_CHUNKS + NTA - 1) / NTA;
     static constexpr int NCU = (U_CHUNKS + NTA - 1) / NTA;
     static constexpr int NCC = (C_CHUNKS + NTA - 1) / NTA;
-    static_assert(TYO % RPT == 0, "rows must split into RPT groups");
+    static_assert(TYO % RPT == 0 && EH % RPTA == 0, "rows must split into RPT groups");
     static_assert(DEPTH >= 6 && ZD >= 3, "rings too shallow");
     template <int KB> static constexpr int NTV = KB == K_A ? 2 : 1;
     template <int KB> static constexpr int ZS_ELEMS = Z_ELEMS + NTV<KB> * T_ELEMS;
@@ -84,9 +85,9 @@ template <int TYO_, int DEPTH_, int ZD_, int MINB_> struct FusedCfg {
                                  size_t(ZD) * ZS_ELEMS<KB>);
     }
 };
-using Fused0 = FusedCfg<16, 6, 4, 1>;
-using Fused1 = FusedCfg<16, 6, 5, 1>;
-using Fused2 = FusedCfg<16, 7, 4, 1>;
+using Fused0 = FusedCfg<16, 6, 4, 1, 4>;
+using Fused1 = FusedCfg<16, 6, 4, 1, 2>;   // twice the stage-A warps
+using Fused2 = FusedCfg<32, 6, 3, 1, 4>;   // larger tile, less halo work
 
 // folded 13-point operator, C3 (same order as stencil_kernel)
 struct Weights {
@@ -125,7 +126,7 @@ template <int KB, class C>
 __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, uint64_t *full,
                                               uint64_t *empty, int x0, int y0, int z_begin,
                                               int nz) {
-    constexpr int RPT = C::RPT, DEPTH = C::DEPTH, EW = C::EW, IW = C::IW, TXO = C::TXO,
+    constexpr int RPT = C::RPTA, DEPTH = C::DEPTH, EW = C::EW, IW = C::IW, TXO = C::TXO,
                   ZD = C::ZD, AD = C::AD;
     constexpr int NTV = C::template NTV<KB>, ZS = C::template ZS_ELEMS<KB>;
     double *yring = sm;
@@ -178,10 +179,13 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
     // input element e = plane z_begin-4+e; aux j (K_B) = u on the ext region and
     // acc on the tile at stage-A plane j (physical z_begin-2+j), issued with
     // input element j+4 so both are waited for together.
+    // issue state: plane of the next input element and its ring slot, and of
+    // the next aux element (kept incrementally: no runtime modulo by n)
+    int zin = wrapi(z_begin - 4, n), sin_ = 0, saux = 0;
     auto issue = [&](int e) {
         {
-            const double *src = a.y + size_t(wrapi(z_begin - 4 + e, n)) * nn;
-            double *dst = yring + size_t(e % DEPTH) * C::Y_ELEMS;
+            const double *src = a.y + size_t(zin) * nn;
+            double *dst = yring + size_t(sin_) * C::Y_ELEMS;
 #pragma unroll
             for (int k = 0; k < C::NCY; ++k)
                 if (ysrc[k] >= 0) cp_async16(dst + ydst[k], src + ysrc[k]);
@@ -189,8 +193,12 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
         if constexpr (KB == K_B) {
             const int j = e - 4;
             if (j >= 0 && j < NJ) {
-                const size_t pl = size_t(wrapi(z_begin - 2 + j, n)) * nn;
-                double *dst = aring + size_t(j % AD) * C::AUX_ELEMS;
+                // aux j is at physical plane z_begin-2+j = plane of input element j+2
+                int zaux = zin - 2;
+                if (zaux < 0) zaux += n;
+                const size_t pl = size_t(zaux) * nn;
+                double *dst = aring + size_t(saux) * C::AUX_ELEMS;
+                saux = (saux + 1 == AD) ? 0 : saux + 1;
 #pragma unroll
                 for (int k = 0; k < C::NCU; ++k)
                     if (usrc[k] >= 0) cp_async16(dst + udst[k], a.p0 + pl + usrc[k]);
@@ -201,6 +209,8 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
                 }
             }
         }
+        zin = (zin + 1 == n) ? 0 : zin + 1;
+        sin_ = (sin_ + 1 == DEPTH) ? 0 : sin_ + 1;
     };
 #pragma unroll 1
     for (int e = 0; e < DEPTH; ++e) {
@@ -241,6 +251,7 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
         for (int r = 0; r < RPT; ++r) q[r][e] = ys[r * IW];
     }
 
+    int s4 = 4 % DEPTH, s2 = 2, szs = 0, sau = 0;  // slots of elements j+4, j+2; Z slot; aux slot
 #pragma unroll 1
     for (int j = 0; j < NJ; ++j) {
         if (j + 4 >= DEPTH + 2) cp_async_wait<DEPTH - 4>();
@@ -249,10 +260,10 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
         while (e_next < E && e_next - DEPTH <= j + 1) issue(e_next++);
         cp_async_commit();
 
-        const double *yq = yring + size_t((j + 4) % DEPTH) * C::Y_ELEMS + sY;
+        const double *yq = yring + size_t(s4) * C::Y_ELEMS + sY;
 #pragma unroll
         for (int r = 0; r < RPT; ++r) q[r][4] = yq[r * IW];
-        const double *ys = yring + size_t((j + 2) % DEPTH) * C::Y_ELEMS + sY;
+        const double *ys = yring + size_t(s2) * C::Y_ELEMS + sY;
         double col[RPT + 4];
 #pragma unroll
         for (int r = 0; r < RPT + 4; ++r)
@@ -262,10 +273,10 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
         for (int r = 0; r < RPT; ++r)
             k[r] = W.apply(ys + r * IW, col[r], col[r + 1], col[r + 3], col[r + 4], q[r]);
 
-        const int zslot = j % ZD;
+        const int zslot = szs;
         if (j >= ZD) mbar_wait(&empty[zslot], ((j / ZD) & 1) ^ 1);
         double *zs = zring + size_t(zslot) * ZS;
-        const double *au = aring + size_t(j % AD) * C::AUX_ELEMS;
+        const double *au = aring + size_t(sau) * C::AUX_ELEMS;
         const bool outp = j >= 2 && j < nz + 2;
         if (valid) {
 #pragma unroll
@@ -290,6 +301,10 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
         for (int r = 0; r < RPT; ++r)
 #pragma unroll
             for (int o = 0; o < 4; ++o) q[r][o] = q[r][o + 1];
+        s4 = (s4 + 1 == DEPTH) ? 0 : s4 + 1;
+        s2 = (s2 + 1 == DEPTH) ? 0 : s2 + 1;
+        szs = (szs + 1 == ZD) ? 0 : szs + 1;
+        sau = (sau + 1 == AD) ? 0 : sau + 1;
     }
     cp_async_wait<0>();
     (void)NTV;
@@ -320,15 +335,16 @@ __device__ __forceinline__ void stage_b_warps(const StencilArgs &a, double *sm, 
     double *o1 = KB == K_A ? a.o1 + size_t(z_begin) * nn + size_t(y0 + r0) * n + x0 + c : nullptr;
 
     double q[RPT][5];
+    int szs = 0, szc = ZD - 2;  // Z slots of planes j and j-2
 #pragma unroll 1
     for (int j = 0; j < NJ; ++j) {
-        const int zslot = j % ZD;
+        const int zslot = szs;
         mbar_wait(&full[zslot], (j / ZD) & 1);
         const double *zq = zring + size_t(zslot) * ZS + sZ;
 #pragma unroll
         for (int r = 0; r < RPT; ++r) q[r][4] = zq[r * EW];
         if (j >= 4) {  // output plane j-4, centred on Z plane j-2
-            const double *zs = zring + size_t((j - 2) % ZD) * ZS;
+            const double *zs = zring + size_t(szc) * ZS;
             const double *zc = zs + sZ;
             double col[RPT + 4];
 #pragma unroll
@@ -348,11 +364,13 @@ __device__ __forceinline__ void stage_b_warps(const StencilArgs &a, double *sm, 
             o0 += nn;
             if (KB == K_A) o1 += nn;
         }
-        if (j >= 2) mbar_arrive(&empty[(j - 2) % ZD]);
+        if (j >= 2) mbar_arrive(&empty[szc]);
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
 #pragma unroll
             for (int o = 0; o < 4; ++o) q[r][o] = q[r][o + 1];
+        szs = (szs + 1 == ZD) ? 0 : szs + 1;
+        szc = (szc + 1 == ZD) ? 0 : szc + 1;
     }
 }
 
