@@ -60,14 +60,17 @@ template <int TYO_, int DEPTH_, int ZD_, int MINB_, int RPTA_ = 4> struct FusedC
     static constexpr int RPT = 4, RPTA = RPTA_;        // rows per thread: stage B, stage A
     static constexpr int EW = TXO + 4, EH = TYO + 4;   // stage-A (extended) region
     static constexpr int IW = TXO + 8, IH = TYO + 8;   // input region
+    // shared-memory row strides (doubles), padded so that row groups of the
+    // edge-column warps fall into different banks; multiples of 2 (16 B rows)
+    static constexpr int IWS = IW + 2, EWS = EW + 2;
     static constexpr int GA = EH / RPTA, GB = TYO / RPT;  // row groups
     static constexpr int EDGE_ITEMS = 4 * GA;            // ext columns 32..35
     static constexpr int EA = (EDGE_ITEMS + 31) / 32;
     static constexpr int WA = GA + EA, WB = GB;
     static constexpr int NTA = 32 * WA, NTB = 32 * WB, NT = NTA + NTB;
     static constexpr int AD = DEPTH - 2;                 // aux ring (K_B)
-    static constexpr int Y_ELEMS = IH * IW;
-    static constexpr int Z_ELEMS = EH * EW;
+    static constexpr int Y_ELEMS = IH * IWS;
+    static constexpr int Z_ELEMS = EH * EWS;
     static constexpr int T_ELEMS = TYO * TXO;
     static constexpr int AUX_ELEMS = Z_ELEMS + T_ELEMS;  // u on the ext region, acc on the tile
     static constexpr int Y_CHUNKS = IH * (IW / 2);
@@ -126,7 +129,7 @@ template <int KB, class C>
 __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, uint64_t *full,
                                               uint64_t *empty, int x0, int y0, int z_begin,
                                               int nz) {
-    constexpr int RPT = C::RPTA, DEPTH = C::DEPTH, EW = C::EW, IW = C::IW, TXO = C::TXO,
+    constexpr int RPT = C::RPTA, DEPTH = C::DEPTH, EW = C::EWS, IW = C::IWS, TXO = C::TXO,
                   ZD = C::ZD, AD = C::AD;
     constexpr int NTV = C::template NTV<KB>, ZS = C::template ZS_ELEMS<KB>;
     double *yring = sm;
@@ -145,9 +148,9 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
         ysrc[k] = -1;
         ydst[k] = 0;
         if (c < C::Y_CHUNKS) {
-            const int r = c / (IW / 2), cc = c % (IW / 2);
+            const int r = c / (C::IW / 2), cc = c % (C::IW / 2);
             ysrc[k] = wrapi(y0 - 4 + r, n) * n + wrapi(x0 - 4 + 2 * cc, n);
-            ydst[k] = r * IW + 2 * cc;
+            ydst[k] = 8 * (r * IW + 2 * cc);  // bytes
         }
     }
     int usrc[KB == K_B ? C::NCU : 1], udst[KB == K_B ? C::NCU : 1];
@@ -159,9 +162,9 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
             usrc[k] = -1;
             udst[k] = 0;
             if (c < C::U_CHUNKS) {
-                const int r = c / (EW / 2), cc = c % (EW / 2);
+                const int r = c / (C::EW / 2), cc = c % (C::EW / 2);
                 usrc[k] = wrapi(y0 - 2 + r, n) * n + wrapi(x0 - 2 + 2 * cc, n);
-                udst[k] = r * EW + 2 * cc;
+                udst[k] = 8 * (r * EW + 2 * cc);
             }
         }
 #pragma unroll
@@ -172,7 +175,7 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
             if (c < C::C_CHUNKS) {
                 const int r = c / (TXO / 2), cc = c % (TXO / 2);
                 csrc[k] = (y0 + r) * n + x0 + 2 * cc;
-                cdst[k] = C::Z_ELEMS + r * TXO + 2 * cc;
+                cdst[k] = 8 * (C::Z_ELEMS + r * TXO + 2 * cc);
             }
         }
     }
@@ -182,13 +185,14 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
     // issue state: plane of the next input element and its ring slot, and of
     // the next aux element (kept incrementally: no runtime modulo by n)
     int zin = wrapi(z_begin - 4, n), sin_ = 0, saux = 0;
+    const uint32_t yring_s = smem_u32(yring), aring_s = smem_u32(aring);
     auto issue = [&](int e) {
         {
             const double *src = a.y + size_t(zin) * nn;
-            double *dst = yring + size_t(sin_) * C::Y_ELEMS;
+            const uint32_t dst = yring_s + uint32_t(sin_) * (C::Y_ELEMS * 8);
 #pragma unroll
             for (int k = 0; k < C::NCY; ++k)
-                if (ysrc[k] >= 0) cp_async16(dst + ydst[k], src + ysrc[k]);
+                if (ysrc[k] >= 0) cp_async16s(dst + ydst[k], src + ysrc[k]);
         }
         if constexpr (KB == K_B) {
             const int j = e - 4;
@@ -197,15 +201,15 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
                 int zaux = zin - 2;
                 if (zaux < 0) zaux += n;
                 const size_t pl = size_t(zaux) * nn;
-                double *dst = aring + size_t(saux) * C::AUX_ELEMS;
+                const uint32_t dst = aring_s + uint32_t(saux) * (C::AUX_ELEMS * 8);
                 saux = (saux + 1 == AD) ? 0 : saux + 1;
 #pragma unroll
                 for (int k = 0; k < C::NCU; ++k)
-                    if (usrc[k] >= 0) cp_async16(dst + udst[k], a.p0 + pl + usrc[k]);
+                    if (usrc[k] >= 0) cp_async16s(dst + udst[k], a.p0 + pl + usrc[k]);
                 if (j >= 2 && j < nz + 2) {
 #pragma unroll
                     for (int k = 0; k < C::NCC; ++k)
-                        if (csrc[k] >= 0) cp_async16(dst + cdst[k], a.p1 + pl + csrc[k]);
+                        if (csrc[k] >= 0) cp_async16s(dst + cdst[k], a.p1 + pl + csrc[k]);
                 }
             }
         }
@@ -314,7 +318,7 @@ template <int KB, class C>
 __device__ __forceinline__ void stage_b_warps(const StencilArgs &a, double *sm, uint64_t *full,
                                               uint64_t *empty, int x0, int y0, int z_begin,
                                               int nz) {
-    constexpr int RPT = C::RPT, EW = C::EW, TXO = C::TXO, ZD = C::ZD, DEPTH = C::DEPTH,
+    constexpr int RPT = C::RPT, EW = C::EWS, TXO = C::TXO, ZD = C::ZD, DEPTH = C::DEPTH,
                   AD = C::AD;
     constexpr int ZS = C::template ZS_ELEMS<KB>;
     double *zring = sm + size_t(DEPTH) * C::Y_ELEMS + (KB == K_B ? size_t(AD) * C::AUX_ELEMS : 0);
