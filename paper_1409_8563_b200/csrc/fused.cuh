@@ -89,7 +89,7 @@ template <int TYO_, int DEPTH_, int ZD_, int MINB_, int RPTA_ = 4> struct FusedC
     }
 };
 using Fused0 = FusedCfg<16, 6, 4, 1, 4>;
-using Fused1 = FusedCfg<16, 6, 4, 1, 2>;   // twice the stage-A warps
+using Fused1 = FusedCfg<16, 6, 4, 1, 2>;   // twice the stage-A warps (default)
 using Fused2 = FusedCfg<32, 6, 3, 1, 4>;   // larger tile, less halo work
 
 // folded 13-point operator, C3 (same order as stencil_kernel)
