@@ -35,8 +35,7 @@ from synthetic import CONFIGS  # noqa: E402
 
 METRIC = "Parareal speedup vs serial fine at 1/2/4/8 B200; RHS stencil HBM GB/s vs peak"
 UNIT = "fine point-steps/s (serial-equivalent)"
-FINE_BYTES_PER_PT = 128   # one RK4 step, four fused stage passes
-COARSE_BYTES_PER_PT = 16  # one Euler step
+COARSE_BYTES_PER_PT = 16  # one Euler step (the fine step's bytes come from pr_grid_info)
 
 
 def load_peaks():
@@ -47,18 +46,50 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(n):
-    """dram bytes per RK4 step (sum over the 4 stage launches) from the committed
-    ncu --set full summary, if one exists for this grid size."""
+def ncu_traffic(n, path):
+    """dram bytes per RK4 step (sum over its launches) from the committed
+    ncu --set full summary (profiles/ncu_summary.json), if one exists."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     try:
         d = json.load(open(p))
-        v = d.get("fine_step_dram_bytes", {}).get(str(n))
+        v = d.get("fine_step_dram_bytes", {}).get(path, {}).get(str(n))
         return float(v) if v is not None else None
     except Exception:
         return None
+
+
+def time_fine_steps(pr, torch, problem, device, steps=64, four_stage=False):
+    """Device time per RK4 step of pr_fine on a fresh grid (CUDA events on the
+    launching stream, after a warm-up); four_stage=True forces the four-pass path."""
+    old = os.environ.get("PR_F2")
+    if four_stage:
+        os.environ["PR_F2"] = "0"
+    try:
+        g = pr.Grid(problem, device)
+    finally:
+        if four_stage:
+            if old is None:
+                os.environ.pop("PR_F2", None)
+            else:
+                os.environ["PR_F2"] = old
+    n = problem.n
+    u = torch.empty((n, n, n), dtype=torch.float64, device=torch.device("cuda", device))
+    pr.pr_fill_sine(g, u)
+    v = torch.empty_like(u)
+    dt = problem.T / 2 ** 13
+    pr.pr_fine(g, u, v, 0, 16, dt)
+    st = torch.cuda.current_stream(u.device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(u.device)
+    e0.record(st)
+    pr.pr_fine(g, u, v, 0, steps, dt)
+    e1.record(st)
+    torch.cuda.synchronize(u.device)
+    info = pr.pr_grid_info(g)
+    g.destroy()
+    return e0.elapsed_time(e1) / steps, info
 
 
 class ClockSampler:
@@ -281,11 +312,24 @@ def main():
     ms_per_step = max_over_ranks(sum(times) / len(times))
     value = n ** 3 * cfg.Nt / (ms_per_step / 1e3)
 
-    # roofline of the dominant kernel (the fused RK4 stages), measured in the timed region
+    # roofline of the dominant kernel (the RK4 step of F), measured in the timed region
+    info = pr.pr_grid_info(grid)
+    fused = info["fine_kernels_per_step"] == 2
+    fine_bytes = info["fine_bytes_per_point"]
     t_fine_step_ms = max_over_ranks(fine_ms / max(fine_steps, 1))
-    achieved = FINE_BYTES_PER_PT * n ** 3 / (t_fine_step_ms / 1e3) / 1e9
+    achieved = fine_bytes * n ** 3 / (t_fine_step_ms / 1e3) / 1e9
     peak, peak_src = load_peaks()
-    traffic = ncu_traffic(n)
+    traffic = ncu_traffic(n, "fused" if fused else "four_stage")
+    # the four-pass kernels measured in the same run, for comparison
+    alt = None
+    if rank == 0 and fused:
+        t4, _ = time_fine_steps(pr, torch, problem, local, 64, four_stage=True)
+        a4 = 128 * n ** 3 / (t4 / 1e3) / 1e9
+        alt = {"bound": "hbm", "achieved": a4, "peak": peak, "unit": "GB/s", "frac": a4 / peak,
+               "traffic": ncu_traffic(n, "four_stage"),
+               "kernel": "stencil_kernel<1..4>: one fused pass per RK4 stage (4 launches, 128 B/pt)",
+               "algorithmic_bytes_per_launch": 128 * n ** 3, "launch_ms": t4,
+               "note": "alternative F path (PR_F2=0), timed on a separate grid after the timed region"}
 
     # e2e: the same solve through the public API with host buffers (pinned), copies timed
     e2e = None
@@ -346,10 +390,14 @@ def main():
                         "defects": dlist},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "rk4_stage S1..S4 (stencil_kernel<1..4>): one RK4 step = 4 launches",
-                         "algorithmic_bytes_per_launch": FINE_BYTES_PER_PT * n ** 3,
+                         "kernel": ("fused_kernel<K_A>+<K_B>: one RK4 step = 2 launches (stages 1+2, 3+4), "
+                                    f"{fine_bytes} B/pt") if fused else
+                                   f"stencil_kernel<1..4>: one RK4 step = 4 launches, {fine_bytes} B/pt",
+                         "launch": "one RK4 step of F (all its kernels), timed inside the timed region",
+                         "algorithmic_bytes_per_launch": fine_bytes * n ** 3,
                          "launch_ms": t_fine_step_ms, "peak_source": peak_src,
                          "point_steps_per_s": n ** 3 / (t_fine_step_ms / 1e3)},
+            "roofline_four_stage": alt,
             "gpu_launches": int(launches),
             "clocks": clocks,
         }

@@ -99,9 +99,10 @@ pr_status pr_destroy_grid(pr_grid *grid);
 
 /* F_dt (Eq.(fine)): n_steps classical RK4 steps of size dt over global
  * steps [step0, step0 + n_steps), from u_in to u_out.  u_in == u_out is
- * allowed; any other overlap is PR_EINVAL.  n_steps = 0 copies.  Four fused
- * stencil passes per step.  Asynchronous on `stream` for device
- * pointers. */
+ * allowed; any other overlap is PR_EINVAL.  n_steps = 0 copies.  One step is
+ * two fused kernels (stages 1+2 and 3+4, 56 B/point) when n is a multiple of
+ * 32, else four fused stage passes (128 B/point); both give bitwise identical
+ * results.  Asynchronous on `stream` for device pointers. */
 pr_status pr_fine(pr_grid *grid, const double *u_in, double *u_out, int64_t step0,
                   int64_t n_steps, double dt, void *stream);
 
@@ -172,6 +173,20 @@ pr_status pr_plan(int32_t n_slices, int32_t K, int32_t world, int32_t rank, pr_o
  * for the predecessor, [4] coarse + correction in the iterations.
  * `cap` >= 5. */
 pr_status pr_last_timings(pr_grid *grid, double *out, int32_t cap);
+
+/* Static facts about a grid's launch configuration (no GPU work):
+ *   fine_kernels_per_step: 2 (fused S1+S2 / S3+S4 kernels, tile-aligned n) or
+ *                          4 (one fused pass per RK4 stage);
+ *   fine_bytes_per_point:  algorithmic HBM bytes per grid point per RK4 step
+ *                          (56 or 128);
+ *   coarse_bytes_per_point: 16 (one Euler pass). */
+typedef struct {
+    int32_t fine_kernels_per_step;
+    int32_t fine_bytes_per_point;
+    int32_t coarse_bytes_per_point;
+    int32_t sms;
+} pr_grid_info_t;
+pr_status pr_grid_info(const pr_grid *grid, pr_grid_info_t *info);
 
 /* Number of kernels this library has launched (graph nodes included). */
 int64_t pr_kernel_launches(void);

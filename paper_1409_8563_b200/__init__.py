@@ -21,7 +21,7 @@ from ._lib import (PR_NU_STAGE, PR_NU_STEP_START, PR_FLAG_G_IS_F, PrError, OPS,
 __all__ = ["Problem", "PararealCfg", "Grid", "pr_create_grid", "pr_destroy_grid", "pr_fine",
            "pr_coarse", "pr_defect", "pr_fill_sine", "pr_correct", "pr_nccl_unique_id",
            "pr_comm_init", "pr_parareal", "pr_plan", "pr_last_timings", "pr_kernel_launches",
-           "pr_stability_ratio", "pr_last_error", "pr_version", "PrError", "PR_NU_STAGE",
+           "pr_stability_ratio", "pr_last_error", "pr_version", "pr_grid_info", "PrError", "PR_NU_STAGE",
            "PR_NU_STEP_START", "PR_FLAG_G_IS_F", "comm_init_torch"]
 
 
@@ -253,6 +253,12 @@ def pr_last_timings(grid) -> dict:
     out = (ctypes.c_double * 5)()
     _lib.check(_lib.load().pr_last_timings(grid.handle, out, 5))
     return dict(zip(["total_ms", "init_ms", "fine_ms", "wait_ms", "coarse_correct_ms"], list(out)))
+
+
+def pr_grid_info(grid) -> dict:
+    info = _lib.PrGridInfo()
+    _lib.check(_lib.load().pr_grid_info(grid.handle, ctypes.byref(info)))
+    return {f: getattr(info, f) for f, _ in _lib.PrGridInfo._fields_}
 
 
 def pr_kernel_launches() -> int:

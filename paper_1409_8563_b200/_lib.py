@@ -25,7 +25,7 @@ OPS = {1: "G_PREFIX", 2: "G_INIT", 3: "DEFECT0", 4: "F", 5: "RECV", 6: "G", 7: "
 EXPORTS = ["pr_create_grid", "pr_destroy_grid", "pr_fine", "pr_coarse", "pr_defect",
            "pr_fill_sine", "pr_correct", "pr_nccl_unique_id", "pr_comm_init", "pr_parareal",
            "pr_plan", "pr_last_timings", "pr_kernel_launches", "pr_stability_ratio",
-           "pr_last_error", "pr_version"]
+           "pr_last_error", "pr_version", "pr_grid_info"]
 
 
 class PrProblem(ctypes.Structure):
@@ -42,6 +42,11 @@ class PrPararealCfg(ctypes.Structure):
 class PrOp(ctypes.Structure):
     _fields_ = [("op", ctypes.c_int32), ("k", ctypes.c_int32), ("slice", ctypes.c_int32),
                 ("peer", ctypes.c_int32)]
+
+
+class PrGridInfo(ctypes.Structure):
+    _fields_ = [("fine_kernels_per_step", ctypes.c_int32), ("fine_bytes_per_point", ctypes.c_int32),
+                ("coarse_bytes_per_point", ctypes.c_int32), ("sms", ctypes.c_int32)]
 
 
 class PrError(RuntimeError):
@@ -81,6 +86,7 @@ def load() -> ctypes.CDLL:
         "pr_stability_ratio": (st, [ctypes.POINTER(PrProblem), dbl, i32, ctypes.POINTER(dbl)]),
         "pr_last_error": (ctypes.c_char_p, []),
         "pr_version": (ctypes.c_char_p, []),
+        "pr_grid_info": (st, [vp, ctypes.POINTER(PrGridInfo)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -1203,6 +1203,15 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
     return PR_OK;
 }
 
+pr_status pr_grid_info(const pr_grid *g, pr_grid_info_t *info) {
+    if (!g || !info) return fail(PR_EINVAL, "null argument");
+    info->fine_kernels_per_step = g->f2 ? 2 : 4;
+    info->fine_bytes_per_point = g->f2 ? 56 : 128;
+    info->coarse_bytes_per_point = 16;
+    info->sms = g->sms;
+    return PR_OK;
+}
+
 pr_status pr_last_timings(pr_grid *g, double *out, int32_t cap) {
     if (!g || !out || cap < 5) return fail(PR_EINVAL, "bad argument");
     for (int i = 0; i < 5; ++i) out[i] = g->timings[i];
