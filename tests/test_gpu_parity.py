@@ -246,3 +246,26 @@ def test_full_size_steps_vs_oracle(n):
     assert rel(out, oracle.fine(p, u0, 1000, 2, dt)) <= TOL
     pr.pr_coarse(g, dev(u0), out, 500, 3, Dt)
     assert rel(out, oracle.coarse(p, u0, 500, 3, Dt)) <= TOL
+
+
+@pytest.mark.parametrize("f2", ["1", "0"])
+@pytest.mark.parametrize("n", [32, 64, 128])
+def test_run_twice_bitwise(n, f2, monkeypatch):
+    """Determinism (the race check available here: compute-sanitizer is closed on
+    this pool): repeated F, G and Parareal runs give bitwise identical fields."""
+    monkeypatch.setenv("PR_F2", f2)
+    g = pr.Grid(pr.Problem(n, c=PARITY_C, T=0.001))
+    u0 = dev(random_field(n, 40))
+    outs = []
+    for _ in range(3):
+        f = torch.empty_like(u0)
+        c = torch.empty_like(u0)
+        pr.pr_fine(g, u0, f, 0, 19, 1e-6)
+        pr.pr_coarse(g, u0, c, 0, 7, 4e-6)
+        uT = torch.empty_like(u0)
+        d = pr.pr_parareal(g, pr.PararealCfg(4, 2, 4, 2), u0, uT, f)
+        outs.append((f, c, uT, d))
+    for f, c, uT, d in outs[1:]:
+        assert torch.equal(f, outs[0][0]) and torch.equal(c, outs[0][1])
+        assert torch.equal(uT, outs[0][2]) and d == outs[0][3]
+    g.destroy()
