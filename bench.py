@@ -92,6 +92,28 @@ def time_fine_steps(pr, torch, problem, device, steps=64, four_stage=False):
     return e0.elapsed_time(e1) / steps, info
 
 
+class Energy:
+    """GPU energy counter (NVML nvmlDeviceGetTotalEnergyConsumption, mJ) of one device."""
+
+    def __init__(self, index):
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self.h = None
+
+    def read_j(self):
+        if self.h is None:
+            return None
+        try:
+            return self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h) / 1e3
+        except Exception:
+            return None
+
+
 class ClockSampler:
     FIELDS = ["index", "clocks.sm", "clocks.max.sm", "clocks_event_reasons.active",
               "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
@@ -262,15 +284,22 @@ def main():
     dt, Dt = cfg.T / cfg.Nt, cfg.T / cfg.NC
     uref = torch.empty_like(u0) if last else None
     C_f_ms = tau_f = tau_c = 0.0
+    phys = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) \
+        if os.environ.get("CUDA_VISIBLE_DEVICES") else local
+    energy = Energy(phys)
+    Q_s = None
     if last:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         pr.pr_fine(grid, u0, uref, 0, 64, dt)  # warm the graphs and tables
         pr.pr_coarse(grid, u0, uT, 0, 64, Dt)
         torch.cuda.synchronize(dev)
+        j0 = energy.read_j()
         e0.record(stream)
         pr.pr_fine(grid, u0, uref, 0, cfg.Nt, dt)
         e1.record(stream)
         torch.cuda.synchronize(dev)
+        j1 = energy.read_j()
+        Q_s = (j1 - j0) if (j0 is not None and j1 is not None) else None
         C_f_ms = e0.elapsed_time(e1)
         tau_f = C_f_ms / cfg.Nt
         e0.record(stream)
@@ -294,6 +323,7 @@ def main():
     times, fine_ms, fine_steps = [], 0.0, 0
     defects = None
     barrier()
+    q0 = energy.read_j()
     for _ in range(args.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -307,6 +337,10 @@ def main():
         if d is not None:
             defects = d
     barrier()
+    q1 = energy.read_j()
+    Q_p_rank = (q1 - q0) / args.steps if (q0 is not None and q1 is not None) else float("nan")
+    Q_p = sum_over_ranks(Q_p_rank)
+    Q_s = max_over_ranks(Q_s if Q_s is not None else float("nan"))
     launches = sum_over_ranks(pr.pr_kernel_launches() - l0)
     clocks = sampler.stop() if sampler else None
     ms_per_step = max_over_ranks(sum(times) / len(times))
@@ -388,6 +422,11 @@ def main():
                         "C_f_ms": C_f_ms, "C_p_ms": ms_per_step, "tau_f_ms": tf_all,
                         "tau_c_ms": tc_all, "tau_c_over_tau_f": r, "N_c_over_N_f": nc / nf,
                         "defects": dlist},
+            "energy": {"Q_serial_J": Q_s, "Q_parareal_J": Q_p,
+                       "gamma_measured": (Q_p / Q_s) if Q_s and Q_s == Q_s else None,
+                       "gamma_ideal": world / S_meas, "gamma_bound": world / S_bound,
+                       "note": "NVML total-energy counters of the GPUs only (Sec. 2.2.2 Eq.(gamma_expected), "
+                               "P:257-285); Q_parareal summed over ranks per solve, Q_serial = serial fine on one GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": ("fused_kernel<K_A>+<K_B>: one RK4 step = 2 launches (stages 1+2, 3+4), "
