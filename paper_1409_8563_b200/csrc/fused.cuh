@@ -26,6 +26,8 @@
 //     stages run concurrently, stage A up to ZD-2 planes ahead) and store the
 //     outputs to HBM coalesced along x.
 #pragma once
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace prk {
@@ -123,7 +125,46 @@ struct Weights {
         az = fma(wp2[2], q[4], az);
         return fma(w0, q[2], ax) + (ay + az);
     }
+    // same, z queue given as a circular buffer whose oldest entry sits at P
+    template <int P>
+    __device__ __forceinline__ double apply_rot(const double *xr, double ym2, double ym1, double yp1,
+                                                double yp2, const double *q) const {
+        double ax = wm1[0] * xr[-1];
+        ax = fma(wp1[0], xr[1], ax);
+        ax = fma(wm2[0], xr[-2], ax);
+        ax = fma(wp2[0], xr[2], ax);
+        double ay = wm1[1] * ym1;
+        ay = fma(wp1[1], yp1, ay);
+        ay = fma(wm2[1], ym2, ay);
+        ay = fma(wp2[1], yp2, ay);
+        double az = wm1[2] * q[(P + 1) % 5];
+        az = fma(wp1[2], q[(P + 3) % 5], az);
+        az = fma(wm2[2], q[P % 5], az);
+        az = fma(wp2[2], q[(P + 4) % 5], az);
+        return fma(w0, q[(P + 2) % 5], ax) + (ay + az);
+    }
 };
+
+template <int P> using Ph = std::integral_constant<int, P>;
+
+// Run body(Ph<j % 5>{}, j) for j = 0 .. NJ-1: the loop is unrolled by five so
+// that z queues indexed with (P + o) % 5 rotate by renaming, not by moves.
+template <class Body>
+__device__ __forceinline__ void rotating_loop(int NJ, Body &&body) {
+    int j = 0;
+#pragma unroll 1
+    for (; j + 5 <= NJ; j += 5) {
+        body(Ph<0>{}, j);
+        body(Ph<1>{}, j + 1);
+        body(Ph<2>{}, j + 2);
+        body(Ph<3>{}, j + 3);
+        body(Ph<4>{}, j + 4);
+    }
+    if (j < NJ) body(Ph<0>{}, j++);
+    if (j < NJ) body(Ph<1>{}, j++);
+    if (j < NJ) body(Ph<2>{}, j++);
+    if (j < NJ) body(Ph<3>{}, j++);
+}
 
 template <int KB, class C>
 __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, uint64_t *full,
@@ -256,8 +297,8 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
     }
 
     int s4 = 4 % DEPTH, s2 = 2, szs = 0, sau = 0;  // slots of elements j+4, j+2; Z slot; aux slot
-#pragma unroll 1
-    for (int j = 0; j < NJ; ++j) {
+    rotating_loop(NJ, [&](auto ph, int j) {
+        constexpr int P = decltype(ph)::value;  // q[r][(P + o) % 5] = plane j-2+o ... (z-2 .. z+2)
         if (j + 4 >= DEPTH + 2) cp_async_wait<DEPTH - 4>();
         else cp_async_wait<DEPTH - 5>();
         named_bar_sync(1, C::NTA);  // element j+4 (+ aux j) visible; slots of j-1 released
@@ -266,16 +307,16 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
 
         const double *yq = yring + size_t(s4) * C::Y_ELEMS + sY;
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) q[r][4] = yq[r * IW];
+        for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = yq[r * IW];
         const double *ys = yring + size_t(s2) * C::Y_ELEMS + sY;
         double col[RPT + 4];
 #pragma unroll
         for (int r = 0; r < RPT + 4; ++r)
-            col[r] = (r >= 2 && r < RPT + 2) ? q[r - 2][2] : ys[(r - 2) * IW];
+            col[r] = (r >= 2 && r < RPT + 2) ? q[r - 2][(P + 2) % 5] : ys[(r - 2) * IW];
         double k[RPT];
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
-            k[r] = W.apply(ys + r * IW, col[r], col[r + 1], col[r + 3], col[r + 4], q[r]);
+            k[r] = W.template apply_rot<P>(ys + r * IW, col[r], col[r + 1], col[r + 3], col[r + 4], q[r]);
 
         const int zslot = szs;
         if (j >= ZD) mbar_wait(&empty[zslot], ((j / ZD) & 1) ^ 1);
@@ -285,7 +326,7 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
         if (valid) {
 #pragma unroll
             for (int r = 0; r < RPT; ++r) {
-                const double yc = q[r][2];
+                const double yc = q[r][(P + 2) % 5];
                 if (KB == K_A) zs[sZ + r * EW] = yc + (dt / 2.0) * k[r];            // Ya
                 else zs[sZ + r * EW] = au[sZ + r * EW] + dt * k[r];                  // Ya'
                 const int er = r0 + r;
@@ -301,15 +342,11 @@ __device__ __forceinline__ void stage_a_warps(const StencilArgs &a, double *sm, 
             }
         }
         mbar_arrive(&full[zslot]);
-#pragma unroll
-        for (int r = 0; r < RPT; ++r)
-#pragma unroll
-            for (int o = 0; o < 4; ++o) q[r][o] = q[r][o + 1];
         s4 = (s4 + 1 == DEPTH) ? 0 : s4 + 1;
         s2 = (s2 + 1 == DEPTH) ? 0 : s2 + 1;
         szs = (szs + 1 == ZD) ? 0 : szs + 1;
         sau = (sau + 1 == AD) ? 0 : sau + 1;
-    }
+    });
     cp_async_wait<0>();
     (void)NTV;
 }
@@ -340,23 +377,24 @@ __device__ __forceinline__ void stage_b_warps(const StencilArgs &a, double *sm, 
 
     double q[RPT][5];
     int szs = 0, szc = ZD - 2;  // Z slots of planes j and j-2
-#pragma unroll 1
-    for (int j = 0; j < NJ; ++j) {
+    rotating_loop(NJ, [&](auto ph, int j) {
+        constexpr int P = decltype(ph)::value;  // q[r][(P + o) % 5] = Z plane j-4+o
         const int zslot = szs;
         mbar_wait(&full[zslot], (j / ZD) & 1);
         const double *zq = zring + size_t(zslot) * ZS + sZ;
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) q[r][4] = zq[r * EW];
+        for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = zq[r * EW];
         if (j >= 4) {  // output plane j-4, centred on Z plane j-2
             const double *zs = zring + size_t(szc) * ZS;
             const double *zc = zs + sZ;
             double col[RPT + 4];
 #pragma unroll
             for (int r = 0; r < RPT + 4; ++r)
-                col[r] = (r >= 2 && r < RPT + 2) ? q[r - 2][2] : zc[(r - 2) * EW];
+                col[r] = (r >= 2 && r < RPT + 2) ? q[r - 2][(P + 2) % 5] : zc[(r - 2) * EW];
 #pragma unroll
             for (int r = 0; r < RPT; ++r) {
-                const double kB = W.apply(zc + r * EW, col[r], col[r + 1], col[r + 3], col[r + 4], q[r]);
+                const double kB = W.template apply_rot<P>(zc + r * EW, col[r], col[r + 1], col[r + 3],
+                                                          col[r + 4], q[r]);
                 const size_t gofs = size_t(r) * n;
                 if (KB == K_A) {
                     o0[gofs] = zs[C::Z_ELEMS + sT + r * TXO] + (dt / 3.0) * kB;                 // acc
@@ -369,13 +407,9 @@ __device__ __forceinline__ void stage_b_warps(const StencilArgs &a, double *sm, 
             if (KB == K_A) o1 += nn;
         }
         if (j >= 2) mbar_arrive(&empty[szc]);
-#pragma unroll
-        for (int r = 0; r < RPT; ++r)
-#pragma unroll
-            for (int o = 0; o < 4; ++o) q[r][o] = q[r][o + 1];
         szs = (szs + 1 == ZD) ? 0 : szs + 1;
         szc = (szc + 1 == ZD) ? 0 : szc + 1;
-    }
+    });
 }
 
 template <int KB, class C>
