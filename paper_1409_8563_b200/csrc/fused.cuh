@@ -58,7 +58,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int count) {
 }
 
 template <int TYO_, int DEPTH_, int ZD_, int MINB_, int RPTA_ = 4> struct FusedCfg {
-    static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = MINB_;
+    static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = MINB_, XP = 1;
     static constexpr int RPT = 4, RPTA = RPTA_;        // rows per thread: stage B, stage A
     static constexpr int EW = TXO + 4, EH = TYO + 4;   // stage-A (extended) region
     static constexpr int IW = TXO + 8, IH = TYO + 8;   // input region
@@ -412,6 +412,330 @@ __device__ __forceinline__ void stage_b_warps(const StencilArgs &a, double *sm, 
     });
 }
 
+
+// ---------------------------------------------------------------------------
+// x-pair variant: every lane owns two adjacent x points (16-byte shared loads
+// and stores).  The 36 extended columns are exactly 18 lane pairs, so there are
+// no edge warps; the floating-point sequence per point is unchanged.
+template <int TYO_, int DEPTH_, int ZD_, int MINB_, int RPTA_, int RPTB_> struct FusedCfgX {
+    static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = MINB_, XP = 2;
+    static constexpr int RPTA = RPTA_, RPT = RPTB_;
+    static constexpr int EW = TXO + 4, EH = TYO + 4, IW = TXO + 8, IH = TYO + 8;
+    static constexpr int IWS = IW + 2, EWS = EW + 2;   // even strides: pairs stay 16-byte aligned
+    static constexpr int GA = EH / RPTA, GB = TYO / RPT;
+    static constexpr int A_ITEMS = (EW / 2) * GA, B_ITEMS = (TXO / 2) * GB;
+    static constexpr int WA = (A_ITEMS + 31) / 32, WB = (B_ITEMS + 31) / 32;
+    static constexpr int NTA = 32 * WA, NTB = 32 * WB, NT = NTA + NTB;
+    static constexpr int AD = DEPTH - 2;
+    static constexpr int Y_ELEMS = IH * IWS, Z_ELEMS = EH * EWS, T_ELEMS = TYO * TXO;
+    static constexpr int AUX_ELEMS = Z_ELEMS + T_ELEMS;
+    static constexpr int Y_CHUNKS = IH * (IW / 2), U_CHUNKS = EH * (EW / 2), C_CHUNKS = TYO * (TXO / 2);
+    static constexpr int NCY = (Y_CHUNKS + NTA - 1) / NTA;
+    static constexpr int NCU = (U_CHUNKS + NTA - 1) / NTA;
+    static constexpr int NCC = (C_CHUNKS + NTA - 1) / NTA;
+    static_assert(TYO % RPT == 0 && EH % RPTA == 0, "rows must split into row groups");
+    static_assert(DEPTH >= 5 && ZD >= 3, "rings too shallow");
+    template <int KB> static constexpr int NTV = KB == K_A ? 2 : 1;
+    template <int KB> static constexpr int ZS_ELEMS = Z_ELEMS + NTV<KB> * T_ELEMS;
+    template <int KB> static constexpr size_t smem_bytes() {
+        return sizeof(double) * (size_t(DEPTH) * Y_ELEMS + (KB == K_B ? size_t(AD) * AUX_ELEMS : 0) +
+                                 size_t(ZD) * ZS_ELEMS<KB>);
+    }
+};
+using Fused3 = FusedCfgX<16, 6, 4, 1, 2, 2>;
+using Fused4 = FusedCfgX<16, 6, 4, 1, 4, 4>;
+using Fused5 = FusedCfgX<32, 5, 3, 1, 4, 4>;
+
+__device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
+__device__ __forceinline__ void sts2(double *p, double2 v) { *reinterpret_cast<double2 *>(p) = v; }
+
+// the folded operator on explicit neighbours, same operation order as Weights::apply
+__device__ __forceinline__ double apply13(const Weights &W, double c, double xm2, double xm1,
+                                          double xp1, double xp2, double ym2, double ym1,
+                                          double yp1, double yp2, double zm2, double zm1,
+                                          double zp1, double zp2) {
+    double ax = W.wm1[0] * xm1;
+    ax = fma(W.wp1[0], xp1, ax);
+    ax = fma(W.wm2[0], xm2, ax);
+    ax = fma(W.wp2[0], xp2, ax);
+    double ay = W.wm1[1] * ym1;
+    ay = fma(W.wp1[1], yp1, ay);
+    ay = fma(W.wm2[1], ym2, ay);
+    ay = fma(W.wp2[1], yp2, ay);
+    double az = W.wm1[2] * zm1;
+    az = fma(W.wp1[2], zp1, az);
+    az = fma(W.wm2[2], zm2, az);
+    az = fma(W.wp2[2], zp2, az);
+    return fma(W.w0, c, ax) + (ay + az);
+}
+
+// both points of a lane pair: L = (x-2, x-1), Cc = (x, x+1), R = (x+2, x+3)
+template <int P>
+__device__ __forceinline__ double2 apply_pair(const Weights &W, double2 L, double2 R, double2 ym2,
+                                              double2 ym1, double2 yp1, double2 yp2,
+                                              const double2 *q) {
+    const double2 Cc = q[(P + 2) % 5];
+    const double2 zm2 = q[P % 5], zm1 = q[(P + 1) % 5], zp1 = q[(P + 3) % 5], zp2 = q[(P + 4) % 5];
+    double2 k;
+    k.x = apply13(W, Cc.x, L.x, L.y, Cc.y, R.x, ym2.x, ym1.x, yp1.x, yp2.x, zm2.x, zm1.x, zp1.x, zp2.x);
+    k.y = apply13(W, Cc.y, L.y, Cc.x, R.x, R.y, ym2.y, ym1.y, yp1.y, yp2.y, zm2.y, zm1.y, zp1.y, zp2.y);
+    return k;
+}
+
+template <int KB, class C>
+__device__ __forceinline__ void stage_a_xp(const StencilArgs &a, double *sm, uint64_t *full,
+                                           uint64_t *empty, int x0, int y0, int z_begin, int nz) {
+    constexpr int RPT = C::RPTA, DEPTH = C::DEPTH, EW = C::EWS, IW = C::IWS, TXO = C::TXO,
+                  ZD = C::ZD, AD = C::AD;
+    constexpr int ZS = C::template ZS_ELEMS<KB>;
+    double *yring = sm;
+    double *aring = yring + size_t(DEPTH) * C::Y_ELEMS;
+    double *zring = aring + (KB == K_B ? size_t(AD) * C::AUX_ELEMS : 0);
+    const int n = a.n;
+    const size_t nn = size_t(n) * n;
+    const int E = nz + 8, NJ = nz + 4;
+    const int t = threadIdx.x;
+
+    int ysrc[C::NCY], ydst[C::NCY];
+#pragma unroll
+    for (int k = 0; k < C::NCY; ++k) {
+        const int c = t + k * C::NTA;
+        ysrc[k] = -1;
+        ydst[k] = 0;
+        if (c < C::Y_CHUNKS) {
+            const int r = c / (C::IW / 2), cc = c % (C::IW / 2);
+            ysrc[k] = wrapi(y0 - 4 + r, n) * n + wrapi(x0 - 4 + 2 * cc, n);
+            ydst[k] = 8 * (r * IW + 2 * cc);
+        }
+    }
+    int usrc[KB == K_B ? C::NCU : 1], udst[KB == K_B ? C::NCU : 1];
+    int csrc[KB == K_B ? C::NCC : 1], cdst[KB == K_B ? C::NCC : 1];
+    if constexpr (KB == K_B) {
+#pragma unroll
+        for (int k = 0; k < C::NCU; ++k) {
+            const int c = t + k * C::NTA;
+            usrc[k] = -1;
+            udst[k] = 0;
+            if (c < C::U_CHUNKS) {
+                const int r = c / (C::EW / 2), cc = c % (C::EW / 2);
+                usrc[k] = wrapi(y0 - 2 + r, n) * n + wrapi(x0 - 2 + 2 * cc, n);
+                udst[k] = 8 * (r * EW + 2 * cc);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < C::NCC; ++k) {
+            const int c = t + k * C::NTA;
+            csrc[k] = -1;
+            cdst[k] = 0;
+            if (c < C::C_CHUNKS) {
+                const int r = c / (TXO / 2), cc = c % (TXO / 2);
+                csrc[k] = (y0 + r) * n + x0 + 2 * cc;
+                cdst[k] = 8 * (C::Z_ELEMS + r * TXO + 2 * cc);
+            }
+        }
+    }
+    int zin = wrapi(z_begin - 4, n), sin_ = 0, saux = 0;
+    const uint32_t yring_s = smem_u32(yring), aring_s = smem_u32(aring);
+    auto issue = [&](int e) {
+        {
+            const double *src = a.y + size_t(zin) * nn;
+            const uint32_t dst = yring_s + uint32_t(sin_) * (C::Y_ELEMS * 8);
+#pragma unroll
+            for (int k = 0; k < C::NCY; ++k)
+                if (ysrc[k] >= 0) cp_async16s(dst + ydst[k], src + ysrc[k]);
+        }
+        if constexpr (KB == K_B) {
+            const int j = e - 4;
+            if (j >= 0 && j < NJ) {
+                int zaux = zin - 2;
+                if (zaux < 0) zaux += n;
+                const size_t pl = size_t(zaux) * nn;
+                const uint32_t dst = aring_s + uint32_t(saux) * (C::AUX_ELEMS * 8);
+                saux = (saux + 1 == AD) ? 0 : saux + 1;
+#pragma unroll
+                for (int k = 0; k < C::NCU; ++k)
+                    if (usrc[k] >= 0) cp_async16s(dst + udst[k], a.p0 + pl + usrc[k]);
+                if (j >= 2 && j < nz + 2) {
+#pragma unroll
+                    for (int k = 0; k < C::NCC; ++k)
+                        if (csrc[k] >= 0) cp_async16s(dst + cdst[k], a.p1 + pl + csrc[k]);
+                }
+            }
+        }
+        zin = (zin + 1 == n) ? 0 : zin + 1;
+        sin_ = (sin_ + 1 == DEPTH) ? 0 : sin_ + 1;
+    };
+#pragma unroll 1
+    for (int e = 0; e < DEPTH; ++e) {
+        if (e < E) issue(e);
+        cp_async_commit();
+    }
+    int e_next = DEPTH;
+
+    const long long row = (*a.nu_pos + a.j_local) * 4;
+    Weights W;
+    W.set(a.nu_tab[row + (KB == K_A ? 0 : 2)], a.inv_dx, a.c);
+    const double dt = a.dt;
+
+    const bool valid = t < C::A_ITEMS;
+    const int l = valid ? t % (C::EW / 2) : 0, g = valid ? t / (C::EW / 2) : 0;
+    const int r0 = g * RPT;                     // first ext row
+    const int sY = (r0 + 2) * IW + 2 * l + 2;   // pair start, first row, input plane
+    const int sZ = r0 * EW + 2 * l;             // same points in a Z / aux-u plane
+    const bool tcol = l >= 1 && l <= TXO / 2;   // both points inside the tile
+    const int tp0 = (r0 - 2) * TXO + 2 * l - 2; // tile offset of row r0 (valid when inside)
+
+    double2 q[RPT][5];
+    cp_async_wait<DEPTH - 4>();
+    named_bar_sync(1, C::NTA);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const double *ys = yring + size_t(e) * C::Y_ELEMS + sY;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) q[r][e] = lds2(ys + r * IW);
+    }
+
+    int s4 = 4 % DEPTH, s2 = 2, szs = 0, sau = 0;
+    rotating_loop(NJ, [&](auto ph, int j) {
+        constexpr int P = decltype(ph)::value;
+        if (j + 4 >= DEPTH + 2) cp_async_wait<DEPTH - 4>();
+        else cp_async_wait<DEPTH - 5>();
+        named_bar_sync(1, C::NTA);
+        while (e_next < E && e_next - DEPTH <= j + 1) issue(e_next++);
+        cp_async_commit();
+
+        const double *yq = yring + size_t(s4) * C::Y_ELEMS + sY;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = lds2(yq + r * IW);
+        const double *ys = yring + size_t(s2) * C::Y_ELEMS + sY;
+        double2 col[RPT + 4];
+#pragma unroll
+        for (int r = 0; r < RPT + 4; ++r)
+            col[r] = (r >= 2 && r < RPT + 2) ? q[r - 2][(P + 2) % 5] : lds2(ys + (r - 2) * IW);
+        double2 k[RPT];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+            k[r] = apply_pair<P>(W, lds2(ys + r * IW - 2), lds2(ys + r * IW + 2), col[r], col[r + 1],
+                                 col[r + 3], col[r + 4], q[r]);
+
+        const int zslot = szs;
+        if (j >= ZD) mbar_wait(&empty[zslot], ((j / ZD) & 1) ^ 1);
+        double *zs = zring + size_t(zslot) * ZS;
+        const double *au = aring + size_t(sau) * C::AUX_ELEMS;
+        const bool outp = j >= 2 && j < nz + 2;
+        if (valid) {
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                const double2 yc = q[r][(P + 2) % 5];
+                double2 z;
+                if (KB == K_A) {
+                    z.x = yc.x + (dt / 2.0) * k[r].x;                         // Ya
+                    z.y = yc.y + (dt / 2.0) * k[r].y;
+                } else {
+                    const double2 ub = lds2(au + sZ + r * EW);
+                    z.x = ub.x + dt * k[r].x;                                 // Ya'
+                    z.y = ub.y + dt * k[r].y;
+                }
+                sts2(zs + sZ + r * EW, z);
+                const int er = r0 + r;
+                if (outp && tcol && er >= 2 && er < C::TYO + 2) {
+                    const int tp = tp0 + r * TXO;
+                    if (KB == K_A) {
+                        double2 t0;
+                        t0.x = yc.x + (dt / 6.0) * k[r].x;                    // u + dt/6 k1
+                        t0.y = yc.y + (dt / 6.0) * k[r].y;
+                        sts2(zs + C::Z_ELEMS + tp, t0);
+                        sts2(zs + C::Z_ELEMS + C::T_ELEMS + tp, yc);          // u
+                    } else {
+                        const double2 ac = lds2(au + C::Z_ELEMS + tp);
+                        double2 t0;
+                        t0.x = ac.x + (dt / 3.0) * k[r].x;                    // acc + dt/3 k3
+                        t0.y = ac.y + (dt / 3.0) * k[r].y;
+                        sts2(zs + C::Z_ELEMS + tp, t0);
+                    }
+                }
+            }
+        }
+        mbar_arrive(&full[zslot]);
+        s4 = (s4 + 1 == DEPTH) ? 0 : s4 + 1;
+        s2 = (s2 + 1 == DEPTH) ? 0 : s2 + 1;
+        szs = (szs + 1 == ZD) ? 0 : szs + 1;
+        sau = (sau + 1 == AD) ? 0 : sau + 1;
+    });
+    cp_async_wait<0>();
+}
+
+template <int KB, class C>
+__device__ __forceinline__ void stage_b_xp(const StencilArgs &a, double *sm, uint64_t *full,
+                                           uint64_t *empty, int x0, int y0, int z_begin, int nz) {
+    constexpr int RPT = C::RPT, EW = C::EWS, TXO = C::TXO, ZD = C::ZD, DEPTH = C::DEPTH,
+                  AD = C::AD;
+    constexpr int ZS = C::template ZS_ELEMS<KB>;
+    double *zring = sm + size_t(DEPTH) * C::Y_ELEMS + (KB == K_B ? size_t(AD) * C::AUX_ELEMS : 0);
+    const int n = a.n;
+    const size_t nn = size_t(n) * n;
+    const int NJ = nz + 4;
+    const int tb = threadIdx.x - C::NTA;
+    const bool valid = tb < C::B_ITEMS;
+    const int m = valid ? tb % (TXO / 2) : 0, g = valid ? tb / (TXO / 2) : 0;
+    const int r0 = g * RPT;                        // first tile row
+    const int sZ = (r0 + 2) * EW + 2 * m + 2;      // pair start, first row, Z plane
+    const int sT = r0 * TXO + 2 * m;
+
+    const long long row = (*a.nu_pos + a.j_local) * 4;
+    Weights W;
+    W.set(a.nu_tab[row + (KB == K_A ? 1 : 3)], a.inv_dx, a.c);
+    const double dt = a.dt;
+    double *o0 = a.o0 + size_t(z_begin) * nn + size_t(y0 + r0) * n + x0 + 2 * m;
+    double *o1 = KB == K_A ? a.o1 + size_t(z_begin) * nn + size_t(y0 + r0) * n + x0 + 2 * m : nullptr;
+
+    double2 q[RPT][5];
+    int szs = 0, szc = ZD - 2;
+    rotating_loop(NJ, [&](auto ph, int j) {
+        constexpr int P = decltype(ph)::value;
+        const int zslot = szs;
+        mbar_wait(&full[zslot], (j / ZD) & 1);
+        const double *zq = zring + size_t(zslot) * ZS + sZ;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = lds2(zq + r * EW);
+        if (j >= 4 && valid) {
+            const double *zs = zring + size_t(szc) * ZS;
+            const double *zc = zs + sZ;
+            double2 col[RPT + 4];
+#pragma unroll
+            for (int r = 0; r < RPT + 4; ++r)
+                col[r] = (r >= 2 && r < RPT + 2) ? q[r - 2][(P + 2) % 5] : lds2(zc + (r - 2) * EW);
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                const double2 kB = apply_pair<P>(W, lds2(zc + r * EW - 2), lds2(zc + r * EW + 2),
+                                                 col[r], col[r + 1], col[r + 3], col[r + 4], q[r]);
+                const size_t gofs = size_t(r) * n;
+                if (KB == K_A) {
+                    const double2 t0 = lds2(zs + C::Z_ELEMS + sT + r * TXO);
+                    const double2 t1 = lds2(zs + C::Z_ELEMS + C::T_ELEMS + sT + r * TXO);
+                    double2 v0, v1;
+                    v0.x = t0.x + (dt / 3.0) * kB.x;  v0.y = t0.y + (dt / 3.0) * kB.y;   // acc
+                    v1.x = t1.x + (dt / 2.0) * kB.x;  v1.y = t1.y + (dt / 2.0) * kB.y;   // Yb
+                    *reinterpret_cast<double2 *>(o0 + gofs) = v0;
+                    *reinterpret_cast<double2 *>(o1 + gofs) = v1;
+                } else {
+                    const double2 t0 = lds2(zs + C::Z_ELEMS + sT + r * TXO);
+                    double2 v0;
+                    v0.x = t0.x + (dt / 6.0) * kB.x;  v0.y = t0.y + (dt / 6.0) * kB.y;   // u_new
+                    *reinterpret_cast<double2 *>(o0 + gofs) = v0;
+                }
+            }
+        }
+        if (j >= 4) {
+            o0 += nn;
+            if (KB == K_A) o1 += nn;
+        }
+        if (j >= 2) mbar_arrive(&empty[szc]);
+        szs = (szs + 1 == ZD) ? 0 : szs + 1;
+        szc = (szc + 1 == ZD) ? 0 : szc + 1;
+    });
+}
+
 template <int KB, class C>
 __global__ void __launch_bounds__(C::NT, C::MINB)
 fused_kernel(const StencilArgs a) {
@@ -431,10 +755,17 @@ fused_kernel(const StencilArgs a) {
         fence_mbar_init();
     }
     __syncthreads();
-    if (threadIdx.x < C::NTA)
-        stage_a_warps<KB, C>(a, sm, full, empty, x0, y0, z_begin, nz);
-    else
-        stage_b_warps<KB, C>(a, sm, full, empty, x0, y0, z_begin, nz);
+    if constexpr (C::XP == 2) {
+        if (threadIdx.x < C::NTA)
+            stage_a_xp<KB, C>(a, sm, full, empty, x0, y0, z_begin, nz);
+        else
+            stage_b_xp<KB, C>(a, sm, full, empty, x0, y0, z_begin, nz);
+    } else {
+        if (threadIdx.x < C::NTA)
+            stage_a_warps<KB, C>(a, sm, full, empty, x0, y0, z_begin, nz);
+        else
+            stage_b_warps<KB, C>(a, sm, full, empty, x0, y0, z_begin, nz);
+    }
 }
 
 }  // namespace prk
