@@ -91,7 +91,7 @@ template <int TYO_, int DEPTH_, int ZD_, int MINB_, int RPTA_ = 4> struct FusedC
     }
 };
 using Fused0 = FusedCfg<16, 6, 4, 1, 4>;
-using Fused1 = FusedCfg<16, 6, 4, 1, 2>;   // twice the stage-A warps (default)
+using Fused1 = FusedCfg<16, 6, 4, 1, 2>;   // twice the stage-A warps
 using Fused2 = FusedCfg<32, 6, 3, 1, 4>;   // larger tile, less halo work
 
 // folded 13-point operator, C3 (same order as stencil_kernel)
@@ -442,7 +442,7 @@ template <int TYO_, int DEPTH_, int ZD_, int MINB_, int RPTA_, int RPTB_> struct
                                  size_t(ZD) * ZS_ELEMS<KB>);
     }
 };
-using Fused3 = FusedCfgX<16, 6, 4, 1, 2, 2>;
+using Fused3 = FusedCfgX<16, 6, 4, 1, 2, 2>;   // default (PR_FTILE=3)
 using Fused4 = FusedCfgX<16, 6, 4, 1, 4, 4>;
 using Fused5 = FusedCfgX<32, 5, 3, 1, 4, 4>;
 
