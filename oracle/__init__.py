@@ -86,6 +86,8 @@ def lib():
             "orc_defect": (dbl, [i32, _D, _D]),
             "orc_parareal": (ctypes.c_int, [P, i32, i32, i32, i32, _D, _D, _D, _D, i32]),
             "orc_threads": (ctypes.c_int, []),
+            "orc_parareal_tol": (ctypes.c_int, [P, i32, i32, i32, i32, dbl, i32, _D, _D, _D, _D, _D,
+                                                ctypes.POINTER(ctypes.c_int32)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -192,6 +194,31 @@ def parareal(p: Problem, n_slices: int, nc: int, nf: int, K: int,
     if rc != 0:
         raise ValueError("orc_parareal: bad arguments")
     return PararealResult(uT, d if u_ref is not None else None)
+
+
+@dataclass
+class PararealTolResult:
+    u_T: np.ndarray
+    defects: np.ndarray
+    changes: np.ndarray   # (world, K) relative iterate change per rank and iteration
+    iters: np.ndarray     # iterations run per rank
+
+
+def parareal_tol(p: Problem, n_slices: int, nc: int, nf: int, K: int, tol: float, world: int,
+                 u0: np.ndarray | None = None, u_ref: np.ndarray | None = None) -> PararealTolResult:
+    """Alg.1 with the convergence-controlled stop rule of DESIGN.md C23."""
+    u0 = initial(p.n) if u0 is None else np.ascontiguousarray(u0, dtype=np.float64)
+    uT = _field(p.n)
+    d = np.full(K + 1, np.nan)
+    ch = np.full(world * K, np.nan)
+    it = (ctypes.c_int32 * world)()
+    pc = p._c()
+    rc = lib().orc_parareal_tol(ctypes.byref(pc), n_slices, nc, nf, K, tol, world, _ptr(u0),
+                                _ptr(np.ascontiguousarray(u_ref)) if u_ref is not None else None,
+                                _ptr(uT), _ptr(d), _ptr(ch), it)
+    if rc != 0:
+        raise ValueError("orc_parareal_tol: bad arguments")
+    return PararealTolResult(uT, d, ch.reshape(world, K), np.array(list(it)))
 
 
 def serial_fine(p: Problem, n_steps_total: int, u0: np.ndarray | None = None) -> np.ndarray:

@@ -320,3 +320,89 @@ int orc_parareal(const orc_problem *p, int32_t n_slices, int32_t nc_, int32_t nf
     free(u_p); free(ut_old); free(msg); free(uhat); free(ut_new); free(u_in);
     return 0;
 }
+
+/* Alg.1 with the stop rule of DESIGN.md C23 (see oracle.h), ranks of s slices
+ * executed in pipeline order: iteration-major, rank-minor. */
+int orc_parareal_tol(const orc_problem *p, int32_t n_slices, int32_t nc_, int32_t nf_, int32_t K,
+                     double tol, int32_t world, const double *u0, const double *u_ref,
+                     double *u_T, double *defects, double *changes, int32_t *iters) {
+    if (!p || !u0 || !u_T || n_slices < 1 || nc_ < 1 || nf_ < 1 || K < 0 || world < 1 ||
+        n_slices % world || p->n < 1 || !(tol >= 0.0))
+        return -1;
+    const int64_t n = p->n, N = n * n * n, Np = n_slices, nc = nc_, nf = nf_, W = world,
+                  s = n_slices / world;
+    const double Dt = p->T / (double)(Np * nc), dt = p->T / (double)(Np * nf);
+    const size_t bytes = sizeof(double) * (size_t)N;
+    double **u_p = (double **)calloc((size_t)Np, sizeof(double *));    /* u^k_j (slice start) */
+    double **ut_old = (double **)calloc((size_t)Np, sizeof(double *)); /* u~^k_{j+1} */
+    double **out = (double **)calloc((size_t)Np, sizeof(double *));    /* u^k_{j+1} (slice end) */
+    double *uhat = alloc_field(n), *ut_new = alloc_field(n), *u_in = alloc_field(n),
+           *neu = alloc_field(n);
+    int *stopped = (int *)calloc((size_t)W, sizeof(int));
+    int ok = u_p && ut_old && out && uhat && ut_new && u_in && neu && stopped;
+    for (int64_t j = 0; ok && j < Np; ++j) {
+        u_p[j] = alloc_field(n);
+        ut_old[j] = alloc_field(n);
+        out[j] = alloc_field(n);
+        ok = u_p[j] && ut_old[j] && out[j];
+    }
+    if (ok) {
+        /* initialisation: rank r's prefix sweeps give the same values as one
+         * serial coarse sweep (same arithmetic per slice) */
+        memcpy(u_p[0], u0, bytes);
+        for (int64_t j = 0; j < Np; ++j) {
+            memcpy(ut_old[j], u_p[j], bytes);
+            G_slice(p, 0, ut_old[j], j, nc, nf, Dt, dt);
+            memcpy(out[j], ut_old[j], bytes);
+            if (j + 1 < Np) memcpy(u_p[j + 1], ut_old[j], bytes);
+        }
+        if (defects && u_ref) {
+            defects[0] = orc_defect(p->n, out[Np - 1], u_ref);
+            for (int32_t k = 1; k <= K; ++k) defects[k] = NAN;
+        }
+        if (changes)
+            for (int64_t i = 0; i < W * K; ++i) changes[i] = NAN;
+        if (iters)
+            for (int64_t r = 0; r < W; ++r) iters[r] = 0;
+        for (int32_t k = 0; k < K; ++k) {
+            for (int64_t r = 0; r < W; ++r) {
+                if (stopped[r]) continue;
+                double dmax = 0.0, umax = 0.0;
+                /* F of every own slice on its old start value, before any update */
+                for (int64_t l = 0; l < s; ++l) {
+                    const int64_t j = r * s + l;
+                    memcpy(uhat, u_p[j], bytes);
+                    F_slice(p, uhat, j, nf, dt);
+                    /* input: u0, the predecessor's value of this iteration (or its
+                     * last one once it stopped), or this rank's previous slice */
+                    if (j == 0) memcpy(u_in, u0, bytes);
+                    else memcpy(u_in, out[j - 1], bytes);
+                    memcpy(ut_new, u_in, bytes);
+                    G_slice(p, 0, ut_new, j, nc, nf, Dt, dt);
+                    for (int64_t q = 0; q < N; ++q) neu[q] = uhat[q] + (ut_new[q] - ut_old[j][q]);
+                    const double dm = orc_inf_diff(p->n, neu, out[j]), um = orc_inf_norm(p->n, neu);
+                    if (dm > dmax || dm != dm) dmax = dm;
+                    if (um > umax) umax = um;
+                    memcpy(ut_old[j], ut_new, bytes);
+                    memcpy(u_p[j], u_in, bytes);
+                    memcpy(out[j], neu, bytes);
+                }
+                const double ch = umax > 0.0 ? dmax / umax : dmax;
+                if (changes) changes[r * K + k] = ch;
+                if (iters) iters[r] = k + 1;
+                const int pred_done = (r == 0) || stopped[r - 1];
+                if (k == K - 1 || (tol > 0.0 && pred_done && ch <= tol)) stopped[r] = 1;
+                if (r == W - 1 && defects && u_ref) defects[k + 1] = orc_defect(p->n, out[Np - 1], u_ref);
+            }
+        }
+        memcpy(u_T, out[Np - 1], bytes);
+    }
+    for (int64_t j = 0; j < Np; ++j) {
+        if (u_p) free(u_p[j]);
+        if (ut_old) free(ut_old[j]);
+        if (out) free(out[j]);
+    }
+    free(u_p); free(ut_old); free(out); free(uhat); free(ut_new); free(u_in); free(neu);
+    free(stopped);
+    return ok ? 0 : -1;
+}

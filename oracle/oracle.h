@@ -80,6 +80,24 @@ int orc_parareal(const orc_problem *p, int32_t n_slices, int32_t nc, int32_t nf,
                  int32_t K, const double *u0, const double *u_ref, double *u_T,
                  double *defects, int32_t flags);
 
+/* Alg.1 with convergence-controlled stopping ("the loop could
+ * alternatively be terminated by checking some convergence criterion", monitor
+ * of P:301-302 "difference between two consecutive iterates"; C23).
+ * `world` ranks own n_slices/world consecutive slices each.  In iteration k a
+ * rank computes its relative iterate change
+ *   c_k = max_l ||u^{k+1}_{l+1} - u^k_{l+1}||_inf / max_l ||u^{k+1}_{l+1}||_inf
+ * over its own slices l (u^0 = the coarse initial guess) and stops after that
+ * iteration when k = K-1, or when its predecessor has stopped (rank 0: always)
+ * and c_k <= tol.  Its message of that iteration carries the stop flag; later
+ * iterations of the successor reuse the last received value.
+ * changes (world*K, may be NULL) receives c_k per rank (NaN when not run),
+ * iters (world, may be NULL) the iterations each rank ran; defects as in
+ * orc_parareal for the iterations the last rank ran (NaN after).  tol <= 0 is
+ * the fixed-K algorithm. */
+int orc_parareal_tol(const orc_problem *p, int32_t n_slices, int32_t nc, int32_t nf, int32_t K,
+                     double tol, int32_t world, const double *u0, const double *u_ref,
+                     double *u_T, double *defects, double *changes, int32_t *iters);
+
 /* Threads the OpenMP runtime will use (1 when built without OpenMP). */
 int orc_threads(void);
 
