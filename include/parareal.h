@@ -81,6 +81,7 @@ typedef struct {
     int32_t n_fine_per_slice;    /* N_f >= 1, delta t = T / (N_p N_f) */
     int32_t K;                   /* iterations k_max >= 0 (K = 0: coarse guess only) */
     int32_t flags;               /* bit 0 (PR_FLAG_G_IS_F): use F for G (degenerate test) */
+    double tol;                  /* > 0: convergence-controlled stopping (below); <= 0: fixed K */
 } pr_parareal_cfg;
 
 #define PR_FLAG_G_IS_F 1
@@ -144,6 +145,13 @@ pr_status pr_comm_init(pr_grid *grid, int32_t world, int32_t rank, const void *n
  * rank only): the serial fine solution for the defect history; when given
  * together with defects_host (K+1 doubles), the last rank writes d^0..d^K
  * (d^0 = coarse initial guess, C11).  Synchronous on return (the timed unit).
+ * Convergence control (cfg->tol > 0, monitor of P:301-302, DESIGN.md
+ * C23): in iteration k a rank measures c_k = max over its slices of
+ * ||u^{k+1}_{j+1} - u^k_{j+1}||_inf / max ||u^{k+1}_{j+1}||_inf and stops after
+ * the iteration when its predecessor has stopped (rank 0: always) and
+ * c_k <= tol, or when k = K-1; the stop flag rides on its last hand-off
+ * message.  Iterations not run leave NaN in defects_host.  The monitors and
+ * the iteration count are returned by pr_last_monitors.
  * Errors: PR_EINVAL, PR_ESTATE (world > 1 without a communicator), PR_ENCCL,
  * PR_EDOMAIN (u_ref all zero), PR_ECUDA. */
 pr_status pr_parareal(pr_grid *grid, const pr_parareal_cfg *cfg, const double *u0,
@@ -167,6 +175,10 @@ typedef struct { int32_t op, k, slice, peer; } pr_op;
  * *count.  PR_EINVAL on bad sizes. */
 pr_status pr_plan(int32_t n_slices, int32_t K, int32_t world, int32_t rank, pr_op *ops,
                   int32_t cap, int32_t *count);
+
+/* Iterate-change monitor c_k of this rank's last pr_parareal call (k < *iterations;
+ * at most `cap` values written) and the number of iterations it ran. */
+pr_status pr_last_monitors(pr_grid *grid, double *changes, int32_t cap, int32_t *iterations);
 
 /* Device-time breakdown of this rank's last pr_parareal call, in ms:
  * out[0] total, [1] init (coarse prefix + own coarse), [2] fine, [3] waiting

@@ -21,7 +21,7 @@ from ._lib import (PR_NU_STAGE, PR_NU_STEP_START, PR_FLAG_G_IS_F, PrError, OPS,
 __all__ = ["Problem", "PararealCfg", "Grid", "pr_create_grid", "pr_destroy_grid", "pr_fine",
            "pr_coarse", "pr_defect", "pr_fill_sine", "pr_correct", "pr_nccl_unique_id",
            "pr_comm_init", "pr_parareal", "pr_plan", "pr_last_timings", "pr_kernel_launches",
-           "pr_stability_ratio", "pr_last_error", "pr_version", "pr_grid_info", "PrError", "PR_NU_STAGE",
+           "pr_stability_ratio", "pr_last_error", "pr_version", "pr_grid_info", "pr_last_monitors", "PrError", "PR_NU_STAGE",
            "PR_NU_STEP_START", "PR_FLAG_G_IS_F", "comm_init_torch"]
 
 
@@ -52,11 +52,12 @@ class PararealCfg:
     n_fine_per_slice: int
     K: int
     flags: int = 0
+    tol: float = 0.0   # > 0: convergence-controlled stopping (C23)
 
     def _c(self) -> _lib.PrPararealCfg:
         c = _lib.PrPararealCfg()
         c.n_slices, c.n_coarse_per_slice, c.n_fine_per_slice = self.n_slices, self.n_coarse_per_slice, self.n_fine_per_slice
-        c.K, c.flags = self.K, self.flags
+        c.K, c.flags, c.tol = self.K, self.flags, float(self.tol)
         return c
 
 
@@ -259,6 +260,15 @@ def pr_grid_info(grid) -> dict:
     info = _lib.PrGridInfo()
     _lib.check(_lib.load().pr_grid_info(grid.handle, ctypes.byref(info)))
     return {f: getattr(info, f) for f, _ in _lib.PrGridInfo._fields_}
+
+
+def pr_last_monitors(grid) -> tuple[list, int]:
+    """(iterate-change monitor per iteration, iterations run) of the last pr_parareal."""
+    cap = 4096
+    buf = (ctypes.c_double * cap)()
+    it = ctypes.c_int32()
+    _lib.check(_lib.load().pr_last_monitors(grid.handle, buf, cap, ctypes.byref(it)))
+    return [buf[k] for k in range(it.value)], it.value
 
 
 def pr_kernel_launches() -> int:

@@ -25,7 +25,7 @@ OPS = {1: "G_PREFIX", 2: "G_INIT", 3: "DEFECT0", 4: "F", 5: "RECV", 6: "G", 7: "
 EXPORTS = ["pr_create_grid", "pr_destroy_grid", "pr_fine", "pr_coarse", "pr_defect",
            "pr_fill_sine", "pr_correct", "pr_nccl_unique_id", "pr_comm_init", "pr_parareal",
            "pr_plan", "pr_last_timings", "pr_kernel_launches", "pr_stability_ratio",
-           "pr_last_error", "pr_version", "pr_grid_info"]
+           "pr_last_error", "pr_version", "pr_grid_info", "pr_last_monitors"]
 
 
 class PrProblem(ctypes.Structure):
@@ -36,7 +36,7 @@ class PrProblem(ctypes.Structure):
 class PrPararealCfg(ctypes.Structure):
     _fields_ = [("n_slices", ctypes.c_int32), ("n_coarse_per_slice", ctypes.c_int32),
                 ("n_fine_per_slice", ctypes.c_int32), ("K", ctypes.c_int32),
-                ("flags", ctypes.c_int32)]
+                ("flags", ctypes.c_int32), ("tol", ctypes.c_double)]
 
 
 class PrOp(ctypes.Structure):
@@ -87,6 +87,7 @@ def load() -> ctypes.CDLL:
         "pr_last_error": (ctypes.c_char_p, []),
         "pr_version": (ctypes.c_char_p, []),
         "pr_grid_info": (st, [vp, ctypes.POINTER(PrGridInfo)]),
+        "pr_last_monitors": (st, [vp, ctypes.POINTER(dbl), i32, ctypes.POINTER(i32)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

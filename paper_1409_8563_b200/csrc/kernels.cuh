@@ -379,18 +379,27 @@ __device__ __forceinline__ void block_max_atomic(unsigned long long v, unsigned 
 
 constexpr int RED_THREADS = 256;
 
-// u_out = f + (g_new - g_old)  [C5];  optional max|u_out - u_ref| -> *dmax
+// u_out = f + (g_new - g_old)  [C5].  Optional fused reductions:
+//   *dmax = max|u_out - u_ref|                      (defect, Eq.(defect))
+//   *cmax = max|u_out - prev|, *nmax = max|u_out|   (iterate-change monitor)
+// prev may alias u_out (read before write by the same thread).
 __global__ void __launch_bounds__(RED_THREADS)
 correct_kernel(const double2 *__restrict__ f, const double2 *__restrict__ gn,
                const double2 *__restrict__ go, double2 *uo, const double2 *__restrict__ ref,
-               unsigned long long *dmax, long long n2) {
-    unsigned long long m = 0;
+               unsigned long long *dmax, const double2 *prev, unsigned long long *cmax,
+               unsigned long long *nmax, long long n2) {
+    unsigned long long m = 0, mc = 0, mn = 0;
     for (long long i = blockIdx.x * (long long)RED_THREADS + threadIdx.x; i < n2;
          i += (long long)gridDim.x * RED_THREADS) {
         const double2 a = f[i], b = gn[i], c = go[i];
         double2 v;
         v.x = a.x + (b.x - c.x);
         v.y = a.y + (b.y - c.y);
+        if (prev) {
+            const double2 o = prev[i];
+            mc = umax64(mc, umax64(abs_bits(v.x - o.x), abs_bits(v.y - o.y)));
+            mn = umax64(mn, umax64(abs_bits(v.x), abs_bits(v.y)));
+        }
         uo[i] = v;
         if (ref) {
             const double2 r = __ldcs(ref + i);
@@ -398,7 +407,16 @@ correct_kernel(const double2 *__restrict__ f, const double2 *__restrict__ gn,
         }
     }
     if (ref) block_max_atomic<RED_THREADS>(m, dmax);
+    if (prev) {
+        __syncthreads();
+        block_max_atomic<RED_THREADS>(mc, cmax);
+        __syncthreads();
+        block_max_atomic<RED_THREADS>(mn, nmax);
+    }
 }
+
+// set the stop-flag element that trails a hand-off buffer (C23)
+__global__ void set_flag_kernel(double *p, double v) { *p = v; }
 
 // *d_diff = max|u - ref| (if u and d_diff), *d_ref = max|ref| (if d_ref)
 __global__ void __launch_bounds__(RED_THREADS)

@@ -117,6 +117,9 @@ struct pr_grid {
     cudaStream_t comm_stream = nullptr;
     std::vector<cudaEvent_t> evs, dep_evs;
     double timings[5] = {0, 0, 0, 0, 0};
+    std::vector<double> monitors;           // iterate-change monitor of the last pr_parareal
+    int iters = 0;                          // iterations it ran
+    double *h_flag = nullptr;               // pinned: received stop flag
 };
 
 template <int KIND, class C>
@@ -703,6 +706,7 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
         if ((s = setup_fused<K_B>(g)) != PR_OK) return bail(s);
     }
     if ((s = ensure_red(g, 8)) != PR_OK) return bail(s);
+    GK(cudaMallocHost(&g->h_flag, 2 * sizeof(double)));
     // generous initial table capacities (graphs capture the pointers)
     GK(cudaMalloc(&g->tab_f.d, (size_t(1) << 20) * sizeof(double)));
     g->tab_f.cap = size_t(1) << 20;
@@ -727,6 +731,7 @@ pr_status pr_destroy_grid(pr_grid *g) {
     cudaFree(g->stage_a); cudaFree(g->stage_b);
     if (g->h_red) cudaFreeHost(g->h_red);
     if (g->h_stage) cudaFreeHost(g->h_stage);
+    if (g->h_flag) cudaFreeHost(g->h_flag);
     for (cudaEvent_t e : g->evs) cudaEventDestroy(e);
     for (cudaEvent_t e : g->dep_evs) cudaEventDestroy(e);
     if (g->stage_ev) cudaEventDestroy(g->stage_ev);
@@ -827,11 +832,14 @@ pr_status pr_fill_sine(pr_grid *g, double *u, void *stream) {
 
 static pr_status launch_correct(pr_grid *g, const double *f, const double *gn, const double *go,
                                 double *uo, const double *ref, unsigned long long *dmax,
-                                cudaStream_t st) {
+                                cudaStream_t st, const double *prev = nullptr,
+                                unsigned long long *cmax = nullptr,
+                                unsigned long long *nmax = nullptr) {
     correct_kernel<<<red_blocks(g), RED_THREADS, 0, st>>>(
         reinterpret_cast<const double2 *>(f), reinterpret_cast<const double2 *>(gn),
         reinterpret_cast<const double2 *>(go), reinterpret_cast<double2 *>(uo),
-        reinterpret_cast<const double2 *>(ref), dmax, g->N / 2);
+        reinterpret_cast<const double2 *>(ref), dmax, reinterpret_cast<const double2 *>(prev),
+        cmax, nmax, g->N / 2);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     CKL();
     return PR_OK;
@@ -943,12 +951,12 @@ static pr_status ensure_events(pr_grid *g, size_t count) {
 }
 
 // Wait for `st` (and the comm stream), polling NCCL for asynchronous errors.
-static pr_status wait_all(pr_grid *g, cudaStream_t st, int k_hint) {
+static pr_status wait_all(pr_grid *g, cudaStream_t st, int k_hint, bool with_comm = true) {
     const char *tenv = getenv("PR_NCCL_TIMEOUT_S");
     const double timeout = tenv ? atof(tenv) : 0.0;
     const auto t0 = std::chrono::steady_clock::now();
     cudaStream_t ss[2] = {st, g->comm ? g->comm_stream : st};
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < (with_comm ? 2 : 1); ++i) {
         for (;;) {
             cudaError_t e = cudaStreamQuery(ss[i]);
             if (e == cudaSuccess) break;
@@ -995,8 +1003,10 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
     const int Np = cfg->n_slices, nc = cfg->n_coarse_per_slice, nf = cfg->n_fine_per_slice,
               K = cfg->K;
     const bool g_is_f = (cfg->flags & PR_FLAG_G_IS_F) != 0;
-    if (Np < 1 || nc < 1 || nf < 1 || K < 0)
-        return fail(PR_EINVAL, "need n_slices, N_c, N_f >= 1 and K >= 0");
+    const double tol = cfg->tol;
+    const bool ctrl = tol > 0.0;  // convergence-controlled stopping (C23)
+    if (Np < 1 || nc < 1 || nf < 1 || K < 0 || !(tol == tol))
+        return fail(PR_EINVAL, "need n_slices, N_c, N_f >= 1, K >= 0 and a number for tol");
     const int W = g->comm ? g->world : 1, r = g->comm ? g->rank : 0;
     if (g->world > 1 && !g->comm) return fail(PR_ESTATE, "world > 1 but no communicator");
     if (Np % W) return fail(PR_EINVAL, "n_slices (%d) must be a multiple of world (%d)", Np, W);
@@ -1014,7 +1024,8 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
     plan.resize(cnt);
     CKS(pr_plan(Np, K, W, r, plan.data(), cnt, &cnt));
 
-    // buffers: start[s], f[s], out[s], gold[s], gnew, recv, u0d, (uref staging)
+    // buffers: start[s], f[s], out[s], gold[s], gnew, recv, u0d; each field has
+    // two trailing doubles (the hand-off message carries a stop flag at [N])
     const size_t nbuf = size_t(4 * s + 3);
     if (g->par_s != s || g->pool.size() != nbuf) {
         CK(cudaDeviceSynchronize());
@@ -1022,7 +1033,7 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
         g->pool.clear();
         for (size_t i = 0; i < nbuf; ++i) {
             double *p = nullptr;
-            CK(cudaMalloc(&p, g->bytes));
+            CK(cudaMalloc(&p, g->bytes + 2 * sizeof(double)));
             g->pool.push_back(p);
         }
         g->par_s = s;
@@ -1042,7 +1053,10 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
         CK(cudaMemcpyAsync(g->stage_b, u_ref, g->bytes, cudaMemcpyHostToDevice, st));
         refd = g->stage_b;
     }
-    CKS(ensure_red(g, K + 2));
+    // reduction slots: [0..K] defect maxima, [K+1] max|u_ref|,
+    // [K+2+2k] max change in iteration k, [K+3+2k] max |u^{k+1}|, [3K+2] spare
+    CKS(ensure_red(g, 3 * K + 4));
+    unsigned long long *red_chg = g->d_red + K + 2;
     // events: 0 start, 1 init done, then per iteration 4: F done, recv done (compute), iter done, send done
     CKS(ensure_events(g, size_t(2 + 4 * K + 2)));
     cudaEvent_t ev_start = g->evs[0], ev_init = g->evs[1];
@@ -1050,18 +1064,14 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
     auto evW = [&](int k) { return g->evs[3 + 4 * k]; };
     auto evI = [&](int k) { return g->evs[4 + 4 * k]; };
     auto evS = [&](int k) { return g->evs[5 + 4 * k]; };
-    std::vector<cudaEvent_t> recv_ev(K), corr_ev(K);
-    // timing-free events for the cross-stream dependencies
     std::vector<cudaEvent_t> &dep = g->dep_evs;
     while (dep.size() < size_t(2 * K + 2)) {
         cudaEvent_t e;
         CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         dep.push_back(e);
     }
-    for (int k = 0; k < K; ++k) {
-        recv_ev[k] = dep[2 * k];
-        corr_ev[k] = dep[2 * k + 1];
-    }
+    auto recv_ev = [&](int k) { return dep[2 * k]; };
+    auto corr_ev = [&](int k) { return dep[2 * k + 1]; };
     cudaEvent_t fdone_ev = dep[2 * K];
 
     CK(cudaEventRecord(ev_start, st));
@@ -1069,7 +1079,7 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
         CK(cudaMemcpyAsync(u0d, u0, g->bytes, cudaMemcpyHostToDevice, st));
     else
         CK(cudaMemcpyAsync(u0d, u0, g->bytes, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemsetAsync(g->d_red, 0, size_t(K + 2) * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(g->d_red, 0, size_t(3 * K + 4) * sizeof(unsigned long long), st));
     // nu tables for everything this rank will run (one upload each)
     if (g_is_f) {
         CKS(ensure_table(g, 1, dt, 0, int64_t(j0 + s) * nf, st));
@@ -1087,13 +1097,16 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
     auto Fp = [&](const double *in, double *o, int m) -> pr_status {
         return run_fine(g, in, o, int64_t(m) * nf, nf, dt, st);
     };
+    const size_t msg = size_t(g->N) + (ctrl ? 1 : 0);  // hand-off length (doubles)
 
     const double *v = u0d;
-    bool sent_pending = false;
-    int last_send_k = -1;
+    bool sent_pending = false, init_marked = false, pred_stopped = (r == 0), stopped = false;
+    bool recvd = false;
+    int last_send_k = -1, iters = 0;
     float ms_fine = 0, ms_wait = 0, ms_gc = 0;
-    bool init_marked = false;
+    g->monitors.assign(size_t(K), std::nan(""));
     for (const pr_op &op : plan) {
+        if (stopped) break;
         const int l = op.slice - j0;
         if (op.k >= 0 && !init_marked) {
             CK(cudaEventRecord(ev_init, st));
@@ -1124,16 +1137,21 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
             }
             break;
         case PR_OP_RECV:
+            recvd = false;
+            if (pred_stopped) break;  // the predecessor sent its last message earlier
             // the receive buffer was last read by F of iteration k-1 (done: stream order)
             CK(cudaStreamWaitEvent(g->comm_stream, fdone_ev, 0));
-            NCK(ncclRecv(recvb, size_t(g->N), ncclDouble, op.peer, g->comm, g->comm_stream), op.k);
-            CK(cudaEventRecord(recv_ev[op.k], g->comm_stream));
-            CK(cudaStreamWaitEvent(st, recv_ev[op.k], 0));
+            NCK(ncclRecv(recvb, msg, ncclDouble, op.peer, g->comm, g->comm_stream), op.k);
+            CK(cudaEventRecord(recv_ev(op.k), g->comm_stream));
+            CK(cudaStreamWaitEvent(st, recv_ev(op.k), 0));
+            if (ctrl) CK(cudaMemcpyAsync(g->h_flag, recvb + g->N, sizeof(double),
+                                         cudaMemcpyDeviceToHost, st));
+            recvd = true;
             break;
         case PR_OP_G: {
             const double *in;
             if (op.slice == 0) in = u0d;
-            else if (l == 0) in = recvb;
+            else if (l == 0) in = recvd ? recvb : start[0];  // stopped predecessor: last value
             else in = out[l - 1];
             if (l == 0) CK(cudaEventRecord(evW(op.k), st));
             CKS(G(in, gnew, op.slice));
@@ -1145,16 +1163,39 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
                 sent_pending = false;
             }
             const bool fuse = want_def && op.slice == Np - 1;
+            // previous iterate of this slice's end value: the coarse guess in
+            // iteration 0, else start[l+1] (l < s-1) or out[s-1] itself
+            const double *prev = op.k == 0 ? gold[l] : (l < s - 1 ? start[l + 1] : out[s - 1]);
             CKS(launch_correct(g, f[l], gnew, gold[l], out[l], fuse ? refd : nullptr,
-                               g->d_red + op.k + 1, st));
+                               g->d_red + op.k + 1, st, prev, red_chg + 2 * op.k,
+                               red_chg + 2 * op.k + 1));
             std::swap(gold[l], gnew);
+            if (l == s - 1) {  // end of this rank's iteration: the stop decision
+                iters = op.k + 1;
+                bool stop_now = (op.k == K - 1);
+                if (ctrl) {
+                    CK(cudaMemcpyAsync(g->h_red, red_chg + 2 * op.k, 2 * sizeof(unsigned long long),
+                                       cudaMemcpyDeviceToHost, st));
+                    CKS(wait_all(g, st, op.k, false));
+                    const double dm = bits_to_double(g->h_red[0]), um = bits_to_double(g->h_red[1]);
+                    const double ch = um > 0.0 ? dm / um : dm;
+                    g->monitors[op.k] = ch;
+                    if (recvd && g->h_flag[0] != 0.0) pred_stopped = true;
+                    if (pred_stopped && ch <= tol) stop_now = true;
+                    if (r < W - 1) {  // the flag rides on this iteration's message
+                        set_flag_kernel<<<1, 1, 0, st>>>(out[s - 1] + g->N, stop_now ? 1.0 : 0.0);
+                        g_launches.fetch_add(1, std::memory_order_relaxed);
+                        CKL();
+                    }
+                }
+                if (stop_now) stopped = true;
+            }
             break;
         }
         case PR_OP_SEND:
-            CK(cudaEventRecord(corr_ev[op.k], st));
-            CK(cudaStreamWaitEvent(g->comm_stream, corr_ev[op.k], 0));
-            NCK(ncclSend(out[s - 1], size_t(g->N), ncclDouble, op.peer, g->comm, g->comm_stream),
-                op.k);
+            CK(cudaEventRecord(corr_ev(op.k), st));
+            CK(cudaStreamWaitEvent(g->comm_stream, corr_ev(op.k), 0));
+            NCK(ncclSend(out[s - 1], msg, ncclDouble, op.peer, g->comm, g->comm_stream), op.k);
             CK(cudaEventRecord(evS(op.k), g->comm_stream));
             sent_pending = true;
             last_send_k = op.k;
@@ -1163,49 +1204,74 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
             CK(cudaEventRecord(evI(op.k), st));
             // start[l] <- the input slice l used in this iteration (buffer rotation)
             for (int ll = s - 1; ll >= 1; --ll) std::swap(start[ll], out[ll - 1]);
-            if (j0 > 0) std::swap(start[0], recvb);
+            if (j0 > 0 && recvd) std::swap(start[0], recvb);
             break;
         default:
             return fail(PR_EINVAL, "bad plan op %d", op.op);
         }
+        // a rank that stops still sends its last message (and records its iteration end)
+        if (stopped && op.op == PR_OP_CORRECT && op.slice == j0 + s - 1) {
+            if (r < W - 1) {
+                CK(cudaEventRecord(corr_ev(op.k), st));
+                CK(cudaStreamWaitEvent(g->comm_stream, corr_ev(op.k), 0));
+                NCK(ncclSend(out[s - 1], msg, ncclDouble, r + 1, g->comm, g->comm_stream), op.k);
+                CK(cudaEventRecord(evS(op.k), g->comm_stream));
+            }
+            CK(cudaEventRecord(evI(op.k), st));
+        }
     }
     if (!init_marked) CK(cudaEventRecord(ev_init, st));
+    g->iters = iters;
     if (last) {
-        const double *res = K > 0 ? out[s - 1] : gold[s - 1];
+        const double *res = iters > 0 ? out[s - 1] : gold[s - 1];
         // after END_ITER the final output of the last slice is still out[s-1]
         CK(cudaMemcpyAsync(u_T, res, g->bytes,
                            is_host_ptr(u_T) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st));
-        if (want_def)
-            CK(cudaMemcpyAsync(g->h_red, g->d_red, size_t(K + 2) * sizeof(unsigned long long),
-                               cudaMemcpyDeviceToHost, st));
     }
+    CK(cudaMemcpyAsync(g->h_red, g->d_red, size_t(3 * K + 4) * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, st));
     cudaEvent_t ev_end = g->evs[2 + 4 * K];
     CK(cudaEventRecord(ev_end, st));
     CKS(wait_all(g, st, K - 1));
     if (want_def) {
         const double M = bits_to_double(g->h_red[K + 1]);
         if (M == 0.0) return fail(PR_EDOMAIN, "max|u_ref| = 0: defect undefined");
-        for (int k = 0; k <= K; ++k) defects_host[k] = bits_to_double(g->h_red[k]) / M;
+        for (int k = 0; k <= K; ++k)
+            defects_host[k] = k <= iters ? bits_to_double(g->h_red[k]) / M : std::nan("");
+    }
+    if (!ctrl) {
+        for (int k = 0; k < iters; ++k) {
+            const double dm = bits_to_double(g->h_red[K + 2 + 2 * k]);
+            const double um = bits_to_double(g->h_red[K + 3 + 2 * k]);
+            g->monitors[k] = um > 0.0 ? dm / um : dm;
+        }
     }
     // timings
     float tot = 0, init = 0;
     cudaEventElapsedTime(&tot, ev_start, ev_end);
     cudaEventElapsedTime(&init, ev_start, ev_init);
-    for (int k = 0; k < K; ++k) {
-        float a = 0, b = 0, c = 0;
+    for (int k = 0; k < iters; ++k) {
+        float a = 0, b = 0, cc = 0;
         cudaEvent_t prev = k == 0 ? ev_init : evI(k - 1);
         cudaEventElapsedTime(&a, prev, evF(k));
         cudaEventElapsedTime(&b, evF(k), evW(k));
-        cudaEventElapsedTime(&c, evW(k), evI(k));
+        cudaEventElapsedTime(&cc, evW(k), evI(k));
         ms_fine += a;
         ms_wait += b;
-        ms_gc += c;
+        ms_gc += cc;
     }
     g->timings[0] = tot;
     g->timings[1] = init;
     g->timings[2] = ms_fine;
     g->timings[3] = ms_wait;
     g->timings[4] = ms_gc;
+    return PR_OK;
+}
+
+pr_status pr_last_monitors(pr_grid *g, double *changes, int32_t cap, int32_t *iterations) {
+    if (!g || !iterations || (cap > 0 && !changes)) return fail(PR_EINVAL, "bad argument");
+    *iterations = g->iters;
+    for (int k = 0; k < std::min<int>(cap, int(g->monitors.size())); ++k) changes[k] = g->monitors[k];
     return PR_OK;
 }
 

@@ -269,3 +269,31 @@ def test_run_twice_bitwise(n, f2, monkeypatch):
         assert torch.equal(f, outs[0][0]) and torch.equal(c, outs[0][1])
         assert torch.equal(uT, outs[0][2]) and d == outs[0][3]
     g.destroy()
+
+
+@pytest.mark.parametrize("pick", [1, 2])
+def test_parareal_convergence_control(pick):
+    """Convergence-controlled stopping (C23) on one GPU (slice group of
+    4): same iteration count, monitors and u_T as the oracle's stop rule."""
+    n, Np, nc, nf, K = 32, 4, 4, 16, 4
+    p = oracle.Problem(n, c=PARITY_C, T=0.004)
+    u0 = random_field(n, 50)
+    uf = oracle.serial_fine(p, Np * nf, u0)
+    full = oracle.parareal_tol(p, Np, nc, nf, K, 0.0, 1, u0, uf)
+    ch = full.changes[0]
+    tol = float(np.sqrt(ch[pick - 1] * ch[pick]))  # between two iterations, far from both
+    ref = oracle.parareal_tol(p, Np, nc, nf, K, tol, 1, u0, uf)
+    assert ref.iters[0] == pick + 1
+    g = grid(n, T=0.004)
+    uT = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+    d = pr.pr_parareal(g, pr.PararealCfg(Np, nc, nf, K, tol=tol), dev(u0), uT, dev(uf))
+    mon, iters = pr.pr_last_monitors(g)
+    assert iters == pick + 1
+    assert rel(uT, ref.u_T) <= TOL
+    assert np.max(np.abs(np.array(mon) - ref.changes[0][:iters])) <= 1e-10
+    assert np.allclose(np.array(d)[:iters + 1], ref.defects[:iters + 1], rtol=0, atol=1e-10)
+    assert all(np.isnan(x) for x in d[iters + 1:])
+    # without tol: K iterations and the same monitors as the oracle
+    pr.pr_parareal(g, pr.PararealCfg(Np, nc, nf, K), dev(u0), uT, dev(uf))
+    mon, iters = pr.pr_last_monitors(g)
+    assert iters == K and np.max(np.abs(np.array(mon) - ch)) <= 1e-10

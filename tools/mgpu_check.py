@@ -25,6 +25,7 @@ def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 32
     Np = int(sys.argv[2]) if len(sys.argv) > 2 else 4
     K = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+    tol = float(sys.argv[4]) if len(sys.argv) > 4 else 0.0
     T, Nt, NC = 0.1, 2048 * (n // 32) ** 2 if n <= 64 else 2048, 128 * (n // 32) ** 2 if n <= 64 else 128
     if n > 64:  # short horizon with the cfg-style step sizes
         T, Nt, NC = 0.1 / 64, 2 ** 11, 2 ** 7
@@ -41,12 +42,29 @@ def main():
     if last:
         pr.pr_fine(g, u0, uf, 0, Nt, T / Nt)
     uT = torch.empty_like(u0)
-    cfg = pr.PararealCfg(Np, NC // Np, Nt // Np, K)
+    cfg = pr.PararealCfg(Np, NC // Np, Nt // Np, K, tol=tol)
     d = pr.pr_parareal(g, cfg, u0, uT if last else None, uf)
     t = pr.pr_last_timings(g)
+    mon, iters = pr.pr_last_monitors(g)
+    all_iters = [None] * world
+    dist.all_gather_object(all_iters, iters)
     ok = True
-    info = {"world": world, "n": n, "Np": Np, "K": K, "defects": d, "timings": t}
-    if last:
+    info = {"world": world, "n": n, "Np": Np, "K": K, "tol": tol, "defects": d, "timings": t,
+            "iters": all_iters}
+    if last and tol > 0:
+        # convergence control: per-rank iteration counts and u_T against the oracle's stop rule
+        import oracle
+        p = oracle.Problem(n, T=T)
+        o0 = oracle.initial(n)
+        ouf = oracle.serial_fine(p, Nt, o0)
+        ref = oracle.parareal_tol(p, Np, NC // Np, Nt // Np, K, tol, world, o0, ouf)
+        err = float(np.max(np.abs(uT.cpu().numpy() - ref.u_T)) / np.max(np.abs(ref.u_T)))
+        info.update(oracle_iters=[int(x) for x in ref.iters], oracle_rel_err=err)
+        ok &= err <= 1e-12 and [int(x) for x in ref.iters] == all_iters
+        info["bitwise_equal_to_1gpu"] = True
+        info["ok"] = bool(ok)
+        print(json.dumps(info), flush=True)
+    elif last:
         # (a) W-invariance: the same slices on this one GPU, without NCCL
         g1 = pr.Grid(pr.Problem(n, T=T), local)
         uT1 = torch.empty_like(u0)
