@@ -227,6 +227,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--nu-mode", type=int, default=None)
+    ap.add_argument("--tol", type=float, default=0.0,
+                    help="convergence-controlled stopping tolerance (DESIGN.md C23); 0 = fixed K")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -311,7 +313,7 @@ def main():
     tc_all = max_over_ranks(tau_c)
     C_f_ms = max_over_ranks(C_f_ms)
 
-    pcfg = pr.PararealCfg(Np, nc, nf, K)
+    pcfg = pr.PararealCfg(Np, nc, nf, K, tol=args.tol)
     for _ in range(args.warmup):
         pr.pr_parareal(grid, pcfg, u0, uT if last else None, uref)
     barrier()
@@ -424,7 +426,9 @@ def main():
                         "E_measured": S_meas / Np, "E_bound": S_bound / Np,
                         "C_f_ms": C_f_ms, "C_p_ms": ms_per_step, "tau_f_ms": tf_all,
                         "tau_c_ms": tc_all, "tau_c_over_tau_f": r, "N_c_over_N_f": nc / nf,
-                        "defects": dlist},
+                        "defects": dlist, "tol": args.tol,
+                        "iterations_run": pr.pr_last_monitors(grid)[1],
+                        "iterate_change_monitor": pr.pr_last_monitors(grid)[0]},
             "energy": {"Q_serial_J": Q_s, "Q_parareal_J": Q_p,
                        "gamma_measured": (Q_p / Q_s) if Q_s and Q_s == Q_s else None,
                        "gamma_ideal": world / S_meas, "gamma_bound": world / S_bound,
