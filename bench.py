@@ -335,7 +335,7 @@ def main():
         times.append(e0.elapsed_time(e1))
         tl = pr.pr_last_timings(grid)
         fine_ms += tl["fine_ms"]
-        fine_steps += K * (Np // world) * nf
+        fine_steps += pr.pr_last_monitors(grid)[1] * (Np // world) * nf
         if d is not None:
             defects = d
     barrier()
