@@ -394,8 +394,10 @@ def main():
     from paper_1409_8563_b200 import perfmodel as pm
     r = tc_all / tf_all
     S_meas = C_f_ms / ms_per_step
-    S_bound = pm.speedup_bound(Np, K, nc, nf, tc_all, tf_all)
-    S_ns = pm.speedup_bound_northstar(Np, K, nc, nf, tc_all, tf_all)
+    # Eq.(speedup) with the number of time-parallel processors = GPUs: with s = N_p/W
+    # slices per GPU the same pipelined model gives N_p -> W
+    S_bound = pm.speedup_bound(world, K, nc, nf, tc_all, tf_all)
+    S_ns = pm.speedup_bound_northstar(world, K, nc, nf, tc_all, tf_all)
     dlist = None
     if world > 1:
         obj = [defects]
@@ -423,7 +425,7 @@ def main():
                              "fields L2-resident"},
             "speedup": {"S_measured": S_meas, "S_bound_eq_speedup_P229": S_bound,
                         "frac_of_bound": S_meas / S_bound, "S_bound_northstar_form": S_ns,
-                        "E_measured": S_meas / Np, "E_bound": S_bound / Np,
+                        "E_measured": S_meas / world, "E_bound": S_bound / world,
                         "C_f_ms": C_f_ms, "C_p_ms": ms_per_step, "tau_f_ms": tf_all,
                         "tau_c_ms": tc_all, "tau_c_over_tau_f": r, "N_c_over_N_f": nc / nf,
                         "defects": dlist, "tol": args.tol,
