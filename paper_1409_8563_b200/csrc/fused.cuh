@@ -445,6 +445,8 @@ template <int TYO_, int DEPTH_, int ZD_, int MINB_, int RPTA_, int RPTB_> struct
 using Fused3 = FusedCfgX<16, 6, 4, 1, 2, 2>;   // default (PR_FTILE=3)
 using Fused4 = FusedCfgX<16, 6, 4, 1, 4, 4>;
 using Fused5 = FusedCfgX<32, 5, 3, 1, 4, 4>;
+using Fused6 = FusedCfgX<16, 6, 4, 1, 1, 2>;   // 12 stage-A warps : 4 stage-B warps
+using Fused7 = FusedCfgX<32, 6, 3, 1, 2, 4>;   // 32-row tile, 11 : 4
 
 __device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
 __device__ __forceinline__ void sts2(double *p, double2 v) { *reinterpret_cast<double2 *>(p) = v; }
