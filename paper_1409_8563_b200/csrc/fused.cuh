@@ -50,6 +50,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// arrive on the mbarrier once all of this thread's prior cp.async copies land
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -58,7 +63,8 @@ __device__ __forceinline__ void named_bar_sync(int id, int count) {
 }
 
 template <int TYO_, int DEPTH_, int ZD_, int MINB_, int RPTA_ = 4> struct FusedCfg {
-    static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = MINB_, XP = 1;
+    static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = MINB_, XP = 1,
+                         PROD = 0;
     static constexpr int RPT = 4, RPTA = RPTA_;        // rows per thread: stage B, stage A
     static constexpr int EW = TXO + 4, EH = TYO + 4;   // stage-A (extended) region
     static constexpr int IW = TXO + 8, IH = TYO + 8;   // input region
@@ -417,15 +423,19 @@ __device__ __forceinline__ void stage_b_warps(const StencilArgs &a, double *sm, 
 // x-pair variant: every lane owns two adjacent x points (16-byte shared loads
 // and stores).  The 36 extended columns are exactly 18 lane pairs, so there are
 // no edge warps; the floating-point sequence per point is unchanged.
-template <int TYO_, int DEPTH_, int ZD_, int MINB_, int RPTA_, int RPTB_> struct FusedCfgX {
+template <int TYO_, int DEPTH_, int ZD_, int MINB_, int RPTA_, int RPTB_, int PROD_ = 0>
+struct FusedCfgX {
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = MINB_, XP = 2;
     static constexpr int RPTA = RPTA_, RPT = RPTB_;
+    // PROD = 1: a dedicated producer warp streams every input/aux plane
+    // (cp.async + cp.async.mbarrier.arrive.noinc); stage-A warps only compute
+    static constexpr int PROD = PROD_;
     static constexpr int EW = TXO + 4, EH = TYO + 4, IW = TXO + 8, IH = TYO + 8;
     static constexpr int IWS = IW + 2, EWS = EW + 2;   // even strides: pairs stay 16-byte aligned
     static constexpr int GA = EH / RPTA, GB = TYO / RPT;
     static constexpr int A_ITEMS = (EW / 2) * GA, B_ITEMS = (TXO / 2) * GB;
     static constexpr int WA = (A_ITEMS + 31) / 32, WB = (B_ITEMS + 31) / 32;
-    static constexpr int NTA = 32 * WA, NTB = 32 * WB, NT = NTA + NTB;
+    static constexpr int NTA = 32 * WA, NTB = 32 * WB, NTP = PROD ? 32 : 0, NT = NTA + NTB + NTP;
     static constexpr int AD = DEPTH - 2;
     static constexpr int Y_ELEMS = IH * IWS, Z_ELEMS = EH * EWS, T_ELEMS = TYO * TXO;
     static constexpr int AUX_ELEMS = Z_ELEMS + T_ELEMS;
@@ -447,6 +457,8 @@ using Fused4 = FusedCfgX<16, 6, 4, 1, 4, 4>;
 using Fused5 = FusedCfgX<32, 5, 3, 1, 4, 4>;
 using Fused6 = FusedCfgX<16, 6, 4, 1, 1, 2>;   // 12 stage-A warps : 4 stage-B warps
 using Fused7 = FusedCfgX<32, 6, 3, 1, 2, 4>;   // 32-row tile, 11 : 4
+using Fused8 = FusedCfgX<16, 6, 4, 1, 2, 2, 1>;   // Fused3 + producer warp
+using Fused9 = FusedCfgX<16, 7, 4, 1, 2, 2, 1>;   // same, deeper input ring
 
 __device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
 __device__ __forceinline__ void sts2(double *p, double2 v) { *reinterpret_cast<double2 *>(p) = v; }
@@ -486,7 +498,8 @@ __device__ __forceinline__ double2 apply_pair(const Weights &W, double2 L, doubl
 
 template <int KB, class C>
 __device__ __forceinline__ void stage_a_xp(const StencilArgs &a, double *sm, uint64_t *full,
-                                           uint64_t *empty, int x0, int y0, int z_begin, int nz) {
+                                           uint64_t *empty, int x0, int y0, int z_begin, int nz,
+                                           uint64_t *in_full, uint64_t *in_empty) {
     constexpr int RPT = C::RPTA, DEPTH = C::DEPTH, EW = C::EWS, IW = C::IWS, TXO = C::TXO,
                   ZD = C::ZD, AD = C::AD;
     constexpr int ZS = C::template ZS_ELEMS<KB>;
@@ -498,7 +511,9 @@ __device__ __forceinline__ void stage_a_xp(const StencilArgs &a, double *sm, uin
     const int E = nz + 8, NJ = nz + 4;
     const int t = threadIdx.x;
 
-    int ysrc[C::NCY], ydst[C::NCY];
+    constexpr bool PROD = C::PROD != 0;
+    int ysrc[PROD ? 1 : C::NCY], ydst[PROD ? 1 : C::NCY];
+    if constexpr (!PROD) {
 #pragma unroll
     for (int k = 0; k < C::NCY; ++k) {
         const int c = t + k * C::NTA;
@@ -510,9 +525,10 @@ __device__ __forceinline__ void stage_a_xp(const StencilArgs &a, double *sm, uin
             ydst[k] = 8 * (r * IW + 2 * cc);
         }
     }
-    int usrc[KB == K_B ? C::NCU : 1], udst[KB == K_B ? C::NCU : 1];
-    int csrc[KB == K_B ? C::NCC : 1], cdst[KB == K_B ? C::NCC : 1];
-    if constexpr (KB == K_B) {
+    }
+    int usrc[KB == K_B && !PROD ? C::NCU : 1], udst[KB == K_B && !PROD ? C::NCU : 1];
+    int csrc[KB == K_B && !PROD ? C::NCC : 1], cdst[KB == K_B && !PROD ? C::NCC : 1];
+    if constexpr (KB == K_B && !PROD) {
 #pragma unroll
         for (int k = 0; k < C::NCU; ++k) {
             const int c = t + k * C::NTA;
@@ -539,14 +555,14 @@ __device__ __forceinline__ void stage_a_xp(const StencilArgs &a, double *sm, uin
     int zin = wrapi(z_begin - 4, n), sin_ = 0, saux = 0;
     const uint32_t yring_s = smem_u32(yring), aring_s = smem_u32(aring);
     auto issue = [&](int e) {
-        {
+        if constexpr (!PROD) {
             const double *src = a.y + size_t(zin) * nn;
             const uint32_t dst = yring_s + uint32_t(sin_) * (C::Y_ELEMS * 8);
 #pragma unroll
             for (int k = 0; k < C::NCY; ++k)
                 if (ysrc[k] >= 0) cp_async16s(dst + ydst[k], src + ysrc[k]);
         }
-        if constexpr (KB == K_B) {
+        if constexpr (KB == K_B && !PROD) {
             const int j = e - 4;
             if (j >= 0 && j < NJ) {
                 int zaux = zin - 2;
@@ -567,12 +583,14 @@ __device__ __forceinline__ void stage_a_xp(const StencilArgs &a, double *sm, uin
         zin = (zin + 1 == n) ? 0 : zin + 1;
         sin_ = (sin_ + 1 == DEPTH) ? 0 : sin_ + 1;
     };
-#pragma unroll 1
-    for (int e = 0; e < DEPTH; ++e) {
-        if (e < E) issue(e);
-        cp_async_commit();
-    }
     int e_next = DEPTH;
+    if constexpr (!PROD) {
+#pragma unroll 1
+        for (int e = 0; e < DEPTH; ++e) {
+            if (e < E) issue(e);
+            cp_async_commit();
+        }
+    }
 
     const long long row = (*a.nu_pos + a.j_local) * 4;
     Weights W;
@@ -588,23 +606,35 @@ __device__ __forceinline__ void stage_a_xp(const StencilArgs &a, double *sm, uin
     const int tp0 = (r0 - 2) * TXO + 2 * l - 2; // tile offset of row r0 (valid when inside)
 
     double2 q[RPT][5];
-    cp_async_wait<DEPTH - 4>();
-    named_bar_sync(1, C::NTA);
+    if constexpr (PROD) {
+        for (int e = 0; e < 4; ++e) mbar_wait(&in_full[e], 0);
+    } else {
+        cp_async_wait<DEPTH - 4>();
+        named_bar_sync(1, C::NTA);
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         const double *ys = yring + size_t(e) * C::Y_ELEMS + sY;
 #pragma unroll
         for (int r = 0; r < RPT; ++r) q[r][e] = lds2(ys + r * IW);
     }
+    if constexpr (PROD) {  // elements 0 and 1 were only needed for the queue
+        mbar_arrive(&in_empty[0]);
+        mbar_arrive(&in_empty[1]);
+    }
 
     int s4 = 4 % DEPTH, s2 = 2, szs = 0, sau = 0;
     rotating_loop(NJ, [&](auto ph, int j) {
         constexpr int P = decltype(ph)::value;
-        if (j + 4 >= DEPTH + 2) cp_async_wait<DEPTH - 4>();
-        else cp_async_wait<DEPTH - 5>();
-        named_bar_sync(1, C::NTA);
-        while (e_next < E && e_next - DEPTH <= j + 1) issue(e_next++);
-        cp_async_commit();
+        if constexpr (PROD) {
+            mbar_wait(&in_full[s4], ((j + 4) / DEPTH) & 1);  // element j+4 (+ aux j) landed
+        } else {
+            if (j + 4 >= DEPTH + 2) cp_async_wait<DEPTH - 4>();
+            else cp_async_wait<DEPTH - 5>();
+            named_bar_sync(1, C::NTA);
+            while (e_next < E && e_next - DEPTH <= j + 1) issue(e_next++);
+            cp_async_commit();
+        }
 
         const double *yq = yring + size_t(s4) * C::Y_ELEMS + sY;
 #pragma unroll
@@ -659,11 +689,106 @@ __device__ __forceinline__ void stage_a_xp(const StencilArgs &a, double *sm, uin
             }
         }
         mbar_arrive(&full[zslot]);
+        if constexpr (PROD) mbar_arrive(&in_empty[s2]);  // element j+2 and aux j are done
         s4 = (s4 + 1 == DEPTH) ? 0 : s4 + 1;
         s2 = (s2 + 1 == DEPTH) ? 0 : s2 + 1;
         szs = (szs + 1 == ZD) ? 0 : szs + 1;
         sau = (sau + 1 == AD) ? 0 : sau + 1;
     });
+    if constexpr (!PROD) cp_async_wait<0>();
+    (void)e_next;
+    (void)E;
+}
+
+// Producer warp (C::PROD): streams input element e (plane z_begin-4+e) and, for
+// K_B, aux element e-4 into the rings; element e may reuse its slot once the
+// stage-A warps released element e-DEPTH (in_empty), and completion is signalled
+// per lane with cp.async.mbarrier.arrive.noinc on in_full (32 arrivals).
+template <int KB, class C>
+__device__ __forceinline__ void producer_xp(const StencilArgs &a, double *sm, int x0, int y0,
+                                            int z_begin, int nz, uint64_t *in_full,
+                                            uint64_t *in_empty) {
+    constexpr int DEPTH = C::DEPTH, EW = C::EWS, IW = C::IWS, TXO = C::TXO, AD = C::AD;
+    constexpr int NY = (C::Y_CHUNKS + 31) / 32, NU = (C::U_CHUNKS + 31) / 32,
+                  NC = (C::C_CHUNKS + 31) / 32;
+    double *yring = sm;
+    double *aring = yring + size_t(DEPTH) * C::Y_ELEMS;
+    const int n = a.n;
+    const size_t nn = size_t(n) * n;
+    const int E = nz + 8, NJ = nz + 4;
+    const int lane = threadIdx.x % 32;
+    int ysrc[NY], ydst[NY];
+#pragma unroll
+    for (int k = 0; k < NY; ++k) {
+        const int c = lane + 32 * k;
+        ysrc[k] = -1;
+        ydst[k] = 0;
+        if (c < C::Y_CHUNKS) {
+            const int r = c / (C::IW / 2), cc = c % (C::IW / 2);
+            ysrc[k] = wrapi(y0 - 4 + r, n) * n + wrapi(x0 - 4 + 2 * cc, n);
+            ydst[k] = 8 * (r * IW + 2 * cc);
+        }
+    }
+    int usrc[KB == K_B ? NU : 1], udst[KB == K_B ? NU : 1];
+    int csrc[KB == K_B ? NC : 1], cdst[KB == K_B ? NC : 1];
+    if constexpr (KB == K_B) {
+#pragma unroll
+        for (int k = 0; k < NU; ++k) {
+            const int c = lane + 32 * k;
+            usrc[k] = -1;
+            udst[k] = 0;
+            if (c < C::U_CHUNKS) {
+                const int r = c / (C::EW / 2), cc = c % (C::EW / 2);
+                usrc[k] = wrapi(y0 - 2 + r, n) * n + wrapi(x0 - 2 + 2 * cc, n);
+                udst[k] = 8 * (r * EW + 2 * cc);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+            const int c = lane + 32 * k;
+            csrc[k] = -1;
+            cdst[k] = 0;
+            if (c < C::C_CHUNKS) {
+                const int r = c / (TXO / 2), cc = c % (TXO / 2);
+                csrc[k] = (y0 + r) * n + x0 + 2 * cc;
+                cdst[k] = 8 * (C::Z_ELEMS + r * TXO + 2 * cc);
+            }
+        }
+    }
+    const uint32_t yring_s = smem_u32(yring), aring_s = smem_u32(aring);
+    int zin = wrapi(z_begin - 4, n), sin_ = 0, saux = 0;
+#pragma unroll 1
+    for (int e = 0; e < E; ++e) {
+        if (e >= DEPTH) mbar_wait(&in_empty[sin_], ((e / DEPTH) - 1) & 1);
+        {
+            const double *src = a.y + size_t(zin) * nn;
+            const uint32_t dst = yring_s + uint32_t(sin_) * (C::Y_ELEMS * 8);
+#pragma unroll
+            for (int k = 0; k < NY; ++k)
+                if (ysrc[k] >= 0) cp_async16s(dst + ydst[k], src + ysrc[k]);
+        }
+        if constexpr (KB == K_B) {
+            const int j = e - 4;
+            if (j >= 0 && j < NJ) {
+                int zaux = zin - 2;
+                if (zaux < 0) zaux += n;
+                const size_t pl = size_t(zaux) * nn;
+                const uint32_t dst = aring_s + uint32_t(saux) * (C::AUX_ELEMS * 8);
+                saux = (saux + 1 == AD) ? 0 : saux + 1;
+#pragma unroll
+                for (int k = 0; k < NU; ++k)
+                    if (usrc[k] >= 0) cp_async16s(dst + udst[k], a.p0 + pl + usrc[k]);
+                if (j >= 2 && j < nz + 2) {
+#pragma unroll
+                    for (int k = 0; k < NC; ++k)
+                        if (csrc[k] >= 0) cp_async16s(dst + cdst[k], a.p1 + pl + csrc[k]);
+                }
+            }
+        }
+        cp_async_mbar_arrive(&in_full[sin_]);
+        zin = (zin + 1 == n) ? 0 : zin + 1;
+        sin_ = (sin_ + 1 == DEPTH) ? 0 : sin_ + 1;
+    }
     cp_async_wait<0>();
 }
 
@@ -743,6 +868,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 fused_kernel(const StencilArgs a) {
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t full[C::ZD], empty[C::ZD];
+    constexpr int NIN = (C::XP == 2 && C::PROD) ? C::DEPTH : 1;
+    __shared__ __align__(8) uint64_t in_full[NIN], in_empty[NIN];
     int b = blockIdx.x;
     const int tix = b % a.tiles_x; b /= a.tiles_x;
     const int tiy = b % a.tiles_y; b /= a.tiles_y;
@@ -754,14 +881,22 @@ fused_kernel(const StencilArgs a) {
             mbar_init(&full[s], C::NTA);
             mbar_init(&empty[s], C::NTB);
         }
+        if constexpr (C::XP == 2 && C::PROD) {
+            for (int s = 0; s < C::DEPTH; ++s) {
+                mbar_init(&in_full[s], 32);
+                mbar_init(&in_empty[s], C::NTA);
+            }
+        }
         fence_mbar_init();
     }
     __syncthreads();
     if constexpr (C::XP == 2) {
         if (threadIdx.x < C::NTA)
-            stage_a_xp<KB, C>(a, sm, full, empty, x0, y0, z_begin, nz);
-        else
+            stage_a_xp<KB, C>(a, sm, full, empty, x0, y0, z_begin, nz, in_full, in_empty);
+        else if (threadIdx.x < C::NTA + C::NTB)
             stage_b_xp<KB, C>(a, sm, full, empty, x0, y0, z_begin, nz);
+        else if constexpr (C::PROD)
+            producer_xp<KB, C>(a, sm, x0, y0, z_begin, nz, in_full, in_empty);
     } else {
         if (threadIdx.x < C::NTA)
             stage_a_warps<KB, C>(a, sm, full, empty, x0, y0, z_begin, nz);

@@ -230,6 +230,8 @@ static pr_status setup_fused(pr_grid *g) {
     case 5: return setup_fused_cfg<KB, Fused5>(g);
     case 6: return setup_fused_cfg<KB, Fused6>(g);
     case 7: return setup_fused_cfg<KB, Fused7>(g);
+    case 8: return setup_fused_cfg<KB, Fused8>(g);
+    case 9: return setup_fused_cfg<KB, Fused9>(g);
     default: return setup_fused_cfg<KB, Fused0>(g);
     }
 }
@@ -250,6 +252,8 @@ static void launch_fused(pr_grid *g, const StencilArgs &a0, cudaStream_t st) {
     case 5: fused_kernel<KB, Fused5><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     case 6: fused_kernel<KB, Fused6><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     case 7: fused_kernel<KB, Fused7><<<c.blocks, c.threads, c.smem, st>>>(a); break;
+    case 8: fused_kernel<KB, Fused8><<<c.blocks, c.threads, c.smem, st>>>(a); break;
+    case 9: fused_kernel<KB, Fused9><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     default: fused_kernel<KB, Fused0><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -702,7 +706,7 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
     if ((s = setup_kind<K_S4>(g)) != PR_OK) return bail(s);
     {
         const char *fe = getenv("PR_F2");
-        if (const char *fv = getenv("PR_FTILE")) g->fvariant = std::max(0, std::min(7, atoi(fv)));
+        if (const char *fv = getenv("PR_FTILE")) g->fvariant = std::max(0, std::min(9, atoi(fv)));
         g->f2 = (n % Fused0::TXO == 0) && (n % Fused0::TYO == 0) && !(fe && fe[0] == '0');
     }
     if (g->f2) {
