@@ -16,12 +16,16 @@
 // Geometry: output tile 32 x TYO (x, y); stage A runs on the extended region
 // 36 x (TYO+4); its input is read on 40 x (TYO+8).  A CTA marches a z chunk.
 // Warp specialisation:
-//   * stage-A warps stream the input planes into a DEPTH-slot shared ring with
-//     16-byte cp.async copies (periodic wrap folded into a per-thread copy plan,
-//     synchronised among themselves by a named barrier), keep z neighbours in
-//     register queues (RPT = 4 consecutive rows per thread), and write each
-//     intermediate plane (Ya or Ya') plus the per-tile-point data stage B needs
-//     into a ZD-slot shared ring;
+//   * a producer warp (default variant) streams the input planes (and K_B's
+//     u/acc planes) into a DEPTH-slot shared ring with 16-byte cp.async copies
+//     (periodic wrap folded into a per-lane copy plan) and signals each plane
+//     with cp.async.mbarrier.arrive.noinc; stage-A warps release slots through
+//     an mbarrier (older variants: stage-A warps issue the copies themselves
+//     and synchronise with a named barrier);
+//   * stage-A warps keep z neighbours in register queues (two adjacent x points
+//     and RPT consecutive rows per thread), and write each intermediate plane
+//     (Ya or Ya') plus the per-tile-point data stage B needs into a ZD-slot
+//     shared ring;
 //   * stage-B warps consume that ring (mbarrier full/empty hand-off, so both
 //     stages run concurrently, stage A up to ZD-2 planes ahead) and store the
 //     outputs to HBM coalesced along x.
@@ -452,13 +456,13 @@ struct FusedCfgX {
                                  size_t(ZD) * ZS_ELEMS<KB>);
     }
 };
-using Fused3 = FusedCfgX<16, 6, 4, 1, 2, 2>;   // default (PR_FTILE=3)
+using Fused3 = FusedCfgX<16, 6, 4, 1, 2, 2>;
 using Fused4 = FusedCfgX<16, 6, 4, 1, 4, 4>;
 using Fused5 = FusedCfgX<32, 5, 3, 1, 4, 4>;
 using Fused6 = FusedCfgX<16, 6, 4, 1, 1, 2>;   // 12 stage-A warps : 4 stage-B warps
 using Fused7 = FusedCfgX<32, 6, 3, 1, 2, 4>;   // 32-row tile, 11 : 4
 using Fused8 = FusedCfgX<16, 6, 4, 1, 2, 2, 1>;   // Fused3 + producer warp
-using Fused9 = FusedCfgX<16, 7, 4, 1, 2, 2, 1>;   // same, deeper input ring
+using Fused9 = FusedCfgX<16, 7, 4, 1, 2, 2, 1>;   // same, deeper input ring (default, PR_FTILE=9)
 
 __device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
 __device__ __forceinline__ void sts2(double *p, double2 v) { *reinterpret_cast<double2 *>(p) = v; }
