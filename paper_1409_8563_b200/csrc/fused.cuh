@@ -909,4 +909,371 @@ fused_kernel(const StencilArgs a) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Persistent variant: one CTA per SM walks work items (tile x z chunk)
+// blockIdx.x, blockIdx.x + gridDim.x, ...  All ring counters run on across
+// items, so the producer warp streams the next item's first planes while the
+// compute warps finish the current one (no per-item pipeline fill).  Aux planes
+// (K_B) share the slot index of the input element they ride with.
+template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_> struct FusedCfgP {
+    static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = 1, XP = 2,
+                         PROD = 1;
+    static constexpr int RPTA = RPTA_, RPT = RPTB_;
+    static constexpr int EW = TXO + 4, EH = TYO + 4, IW = TXO + 8, IH = TYO + 8;
+    static constexpr int IWS = IW + 2, EWS = EW + 2;
+    static constexpr int GA = EH / RPTA, GB = TYO / RPT;
+    static constexpr int A_ITEMS = (EW / 2) * GA, B_ITEMS = (TXO / 2) * GB;
+    static constexpr int WA = (A_ITEMS + 31) / 32, WB = (B_ITEMS + 31) / 32;
+    static constexpr int NTA = 32 * WA, NTB = 32 * WB, NTP = 32, NT = NTA + NTB + NTP;
+    static constexpr int AD = DEPTH;  // aux slots follow the input slots
+    static constexpr int Y_ELEMS = IH * IWS, Z_ELEMS = EH * EWS, T_ELEMS = TYO * TXO;
+    static constexpr int AUX_ELEMS = Z_ELEMS + T_ELEMS;
+    static constexpr int Y_CHUNKS = IH * (IW / 2), U_CHUNKS = EH * (EW / 2), C_CHUNKS = TYO * (TXO / 2);
+    static_assert(TYO % RPT == 0 && EH % RPTA == 0, "rows must split into row groups");
+    static_assert(DEPTH >= 5 && ZD >= 3, "rings too shallow");
+    template <int KB> static constexpr int NTV = KB == K_A ? 2 : 1;
+    template <int KB> static constexpr int ZS_ELEMS = Z_ELEMS + NTV<KB> * T_ELEMS;
+    template <int KB> static constexpr size_t smem_bytes() {
+        return sizeof(double) * (size_t(DEPTH) * Y_ELEMS + (KB == K_B ? size_t(AD) * AUX_ELEMS : 0) +
+                                 size_t(ZD) * ZS_ELEMS<KB>);
+    }
+};
+using FusedP0 = FusedCfgP<16, 7, 4, 2, 2>;
+
+struct WorkItem {
+    int x0, y0, z_begin, nz;
+};
+__device__ __forceinline__ WorkItem decode_item(const StencilArgs &a, int item, int txo, int tyo) {
+    WorkItem w;
+    int b = item;
+    const int tix = b % a.tiles_x; b /= a.tiles_x;
+    const int tiy = b % a.tiles_y; b /= a.tiles_y;
+    w.x0 = tix * txo;
+    w.y0 = tiy * tyo;
+    w.z_begin = b * a.cz;
+    w.nz = min(a.cz, a.n - w.z_begin);
+    return w;
+}
+
+// ring position: slot index and the fill round it belongs to
+struct RingPos {
+    int slot = 0, round = 0;
+    __device__ __forceinline__ void step(int depth) {
+        if (++slot == depth) { slot = 0; ++round; }
+    }
+};
+__device__ __forceinline__ RingPos ring_at(RingPos p, int k, int depth) {
+    for (int i = 0; i < k; ++i) p.step(depth);
+    return p;
+}
+
+template <int KB, class C>
+__device__ __forceinline__ void producer_p(const StencilArgs &a, double *sm, int items,
+                                           uint64_t *in_full, uint64_t *in_empty) {
+    constexpr int DEPTH = C::DEPTH, EW = C::EWS, IW = C::IWS, TXO = C::TXO;
+    constexpr int NY = (C::Y_CHUNKS + 31) / 32, NU = (C::U_CHUNKS + 31) / 32,
+                  NC = (C::C_CHUNKS + 31) / 32;
+    double *yring = sm;
+    double *aring = yring + size_t(DEPTH) * C::Y_ELEMS;
+    const int n = a.n;
+    const size_t nn = size_t(n) * n;
+    const int lane = threadIdx.x % 32;
+    const uint32_t yring_s = smem_u32(yring), aring_s = smem_u32(aring);
+    RingPos pos;
+#pragma unroll 1
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const WorkItem w = decode_item(a, item, TXO, C::TYO);
+        const int E = w.nz + 8, NJ = w.nz + 4;
+        int ysrc[NY], ydst[NY];
+#pragma unroll
+        for (int k = 0; k < NY; ++k) {
+            const int c = lane + 32 * k;
+            ysrc[k] = -1;
+            ydst[k] = 0;
+            if (c < C::Y_CHUNKS) {
+                const int r = c / (C::IW / 2), cc = c % (C::IW / 2);
+                ysrc[k] = wrapi(w.y0 - 4 + r, n) * n + wrapi(w.x0 - 4 + 2 * cc, n);
+                ydst[k] = 8 * (r * IW + 2 * cc);
+            }
+        }
+        int usrc[KB == K_B ? NU : 1], udst[KB == K_B ? NU : 1];
+        int csrc[KB == K_B ? NC : 1], cdst[KB == K_B ? NC : 1];
+        if constexpr (KB == K_B) {
+#pragma unroll
+            for (int k = 0; k < NU; ++k) {
+                const int c = lane + 32 * k;
+                usrc[k] = -1;
+                udst[k] = 0;
+                if (c < C::U_CHUNKS) {
+                    const int r = c / (C::EW / 2), cc = c % (C::EW / 2);
+                    usrc[k] = wrapi(w.y0 - 2 + r, n) * n + wrapi(w.x0 - 2 + 2 * cc, n);
+                    udst[k] = 8 * (r * EW + 2 * cc);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+                const int c = lane + 32 * k;
+                csrc[k] = -1;
+                cdst[k] = 0;
+                if (c < C::C_CHUNKS) {
+                    const int r = c / (TXO / 2), cc = c % (TXO / 2);
+                    csrc[k] = (w.y0 + r) * n + w.x0 + 2 * cc;
+                    cdst[k] = 8 * (C::Z_ELEMS + r * TXO + 2 * cc);
+                }
+            }
+        }
+        int zin = wrapi(w.z_begin - 4, n);
+#pragma unroll 1
+        for (int e = 0; e < E; ++e) {
+            if (pos.round > 0) mbar_wait(&in_empty[pos.slot], (pos.round - 1) & 1);
+            {
+                const double *src = a.y + size_t(zin) * nn;
+                const uint32_t dst = yring_s + uint32_t(pos.slot) * (C::Y_ELEMS * 8);
+#pragma unroll
+                for (int k = 0; k < NY; ++k)
+                    if (ysrc[k] >= 0) cp_async16s(dst + ydst[k], src + ysrc[k]);
+            }
+            if constexpr (KB == K_B) {
+                const int j = e - 4;  // aux j rides with input element j+4
+                if (j >= 0 && j < NJ) {
+                    int zaux = zin - 2;
+                    if (zaux < 0) zaux += n;
+                    const size_t pl = size_t(zaux) * nn;
+                    const uint32_t dst = aring_s + uint32_t(pos.slot) * (C::AUX_ELEMS * 8);
+#pragma unroll
+                    for (int k = 0; k < NU; ++k)
+                        if (usrc[k] >= 0) cp_async16s(dst + udst[k], a.p0 + pl + usrc[k]);
+                    if (j >= 2 && j < w.nz + 2) {
+#pragma unroll
+                        for (int k = 0; k < NC; ++k)
+                            if (csrc[k] >= 0) cp_async16s(dst + cdst[k], a.p1 + pl + csrc[k]);
+                    }
+                }
+            }
+            cp_async_mbar_arrive(&in_full[pos.slot]);
+            zin = (zin + 1 == n) ? 0 : zin + 1;
+            pos.step(DEPTH);
+        }
+    }
+    cp_async_wait<0>();
+}
+
+template <int KB, class C>
+__device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int items,
+                                          uint64_t *full, uint64_t *empty, uint64_t *in_full,
+                                          uint64_t *in_empty) {
+    constexpr int RPT = C::RPTA, DEPTH = C::DEPTH, EW = C::EWS, IW = C::IWS, TXO = C::TXO,
+                  ZD = C::ZD;
+    constexpr int ZS = C::template ZS_ELEMS<KB>;
+    double *yring = sm;
+    double *aring = yring + size_t(DEPTH) * C::Y_ELEMS;
+    double *zring = aring + (KB == K_B ? size_t(C::AD) * C::AUX_ELEMS : 0);
+    const int t = threadIdx.x;
+
+    const long long row = (*a.nu_pos + a.j_local) * 4;
+    Weights W;
+    W.set(a.nu_tab[row + (KB == K_A ? 0 : 2)], a.inv_dx, a.c);
+    const double dt = a.dt;
+
+    const bool valid = t < C::A_ITEMS;
+    const int l = valid ? t % (C::EW / 2) : 0, g = valid ? t / (C::EW / 2) : 0;
+    const int r0 = g * RPT;
+    const int sY = (r0 + 2) * IW + 2 * l + 2;
+    const int sZ = r0 * EW + 2 * l;
+    const bool tcol = l >= 1 && l <= TXO / 2;
+    const int tp0 = (r0 - 2) * TXO + 2 * l - 2;
+
+    RingPos base, zpos;  // input element 0 of the current item; next Z plane
+#pragma unroll 1
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const WorkItem w = decode_item(a, item, TXO, C::TYO);
+        const int NJ = w.nz + 4;
+        double2 q[RPT][5];
+        RingPos p0 = base;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            mbar_wait(&in_full[p0.slot], p0.round & 1);
+            const double *ys = yring + size_t(p0.slot) * C::Y_ELEMS + sY;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) q[r][e] = lds2(ys + r * IW);
+            p0.step(DEPTH);
+        }
+        // elements 0 and 1 were only needed for the queue
+        mbar_arrive(&in_empty[base.slot]);
+        mbar_arrive(&in_empty[ring_at(base, 1, DEPTH).slot]);
+        RingPos p2 = ring_at(base, 2, DEPTH), p4 = p0;  // elements j+2, j+4
+        rotating_loop(NJ, [&](auto ph, int j) {
+            constexpr int P = decltype(ph)::value;
+            mbar_wait(&in_full[p4.slot], p4.round & 1);  // element j+4 (+ aux j) landed
+            const double *yq = yring + size_t(p4.slot) * C::Y_ELEMS + sY;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = lds2(yq + r * IW);
+            const double *ys = yring + size_t(p2.slot) * C::Y_ELEMS + sY;
+            double2 col[RPT + 4];
+#pragma unroll
+            for (int r = 0; r < RPT + 4; ++r)
+                col[r] = (r >= 2 && r < RPT + 2) ? q[r - 2][(P + 2) % 5] : lds2(ys + (r - 2) * IW);
+            double2 k[RPT];
+#pragma unroll
+            for (int r = 0; r < RPT; ++r)
+                k[r] = apply_pair<P>(W, lds2(ys + r * IW - 2), lds2(ys + r * IW + 2), col[r],
+                                     col[r + 1], col[r + 3], col[r + 4], q[r]);
+            if (zpos.round > 0) mbar_wait(&empty[zpos.slot], (zpos.round - 1) & 1);
+            double *zs = zring + size_t(zpos.slot) * ZS;
+            const double *au = aring + size_t(p4.slot) * C::AUX_ELEMS;  // aux j
+            const bool outp = j >= 2 && j < w.nz + 2;
+            if (valid) {
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {
+                    const double2 yc = q[r][(P + 2) % 5];
+                    double2 z;
+                    if (KB == K_A) {
+                        z.x = yc.x + (dt / 2.0) * k[r].x;
+                        z.y = yc.y + (dt / 2.0) * k[r].y;
+                    } else {
+                        const double2 ub = lds2(au + sZ + r * EW);
+                        z.x = ub.x + dt * k[r].x;
+                        z.y = ub.y + dt * k[r].y;
+                    }
+                    sts2(zs + sZ + r * EW, z);
+                    const int er = r0 + r;
+                    if (outp && tcol && er >= 2 && er < C::TYO + 2) {
+                        const int tp = tp0 + r * TXO;
+                        if (KB == K_A) {
+                            double2 t0;
+                            t0.x = yc.x + (dt / 6.0) * k[r].x;
+                            t0.y = yc.y + (dt / 6.0) * k[r].y;
+                            sts2(zs + C::Z_ELEMS + tp, t0);
+                            sts2(zs + C::Z_ELEMS + C::T_ELEMS + tp, yc);
+                        } else {
+                            const double2 ac = lds2(au + C::Z_ELEMS + tp);
+                            double2 t0;
+                            t0.x = ac.x + (dt / 3.0) * k[r].x;
+                            t0.y = ac.y + (dt / 3.0) * k[r].y;
+                            sts2(zs + C::Z_ELEMS + tp, t0);
+                        }
+                    }
+                }
+            }
+            mbar_arrive(&full[zpos.slot]);
+            mbar_arrive(&in_empty[p2.slot]);  // element j+2 done (aux j lives in slot j+4)
+            p2.step(DEPTH);
+            p4.step(DEPTH);
+            zpos.step(ZD);
+        });
+        // the item's last two input elements were only used by the queue
+        mbar_arrive(&in_empty[p2.slot]);
+        mbar_arrive(&in_empty[ring_at(p2, 1, DEPTH).slot]);
+        base = ring_at(p2, 2, DEPTH);
+    }
+}
+
+template <int KB, class C>
+__device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int items,
+                                          uint64_t *full, uint64_t *empty) {
+    constexpr int RPT = C::RPT, EW = C::EWS, TXO = C::TXO, ZD = C::ZD, DEPTH = C::DEPTH;
+    constexpr int ZS = C::template ZS_ELEMS<KB>;
+    double *zring = sm + size_t(DEPTH) * C::Y_ELEMS + (KB == K_B ? size_t(C::AD) * C::AUX_ELEMS : 0);
+    const int n = a.n;
+    const size_t nn = size_t(n) * n;
+    const int tb = threadIdx.x - C::NTA;
+    const bool valid = tb < C::B_ITEMS;
+    const int m = valid ? tb % (TXO / 2) : 0, g = valid ? tb / (TXO / 2) : 0;
+    const int r0 = g * RPT;
+    const int sZ = (r0 + 2) * EW + 2 * m + 2;
+    const int sT = r0 * TXO + 2 * m;
+
+    const long long row = (*a.nu_pos + a.j_local) * 4;
+    Weights W;
+    W.set(a.nu_tab[row + (KB == K_A ? 1 : 3)], a.inv_dx, a.c);
+    const double dt = a.dt;
+
+    RingPos zq_pos;  // Z plane j of the current item
+#pragma unroll 1
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const WorkItem w = decode_item(a, item, TXO, C::TYO);
+        const int NJ = w.nz + 4;
+        double *o0 = a.o0 + size_t(w.z_begin) * nn + size_t(w.y0 + r0) * n + w.x0 + 2 * m;
+        double *o1 = KB == K_A ? a.o1 + size_t(w.z_begin) * nn + size_t(w.y0 + r0) * n + w.x0 + 2 * m
+                               : nullptr;
+        double2 q[RPT][5];
+        RingPos zc_pos = zq_pos;  // Z plane j-2 (valid from j = 2)
+        rotating_loop(NJ, [&](auto ph, int j) {
+            constexpr int P = decltype(ph)::value;
+            mbar_wait(&full[zq_pos.slot], zq_pos.round & 1);
+            const double *zq = zring + size_t(zq_pos.slot) * ZS + sZ;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = lds2(zq + r * EW);
+            if (j >= 4 && valid) {
+                const double *zs = zring + size_t(zc_pos.slot) * ZS;
+                const double *zc = zs + sZ;
+                double2 col[RPT + 4];
+#pragma unroll
+                for (int r = 0; r < RPT + 4; ++r)
+                    col[r] = (r >= 2 && r < RPT + 2) ? q[r - 2][(P + 2) % 5] : lds2(zc + (r - 2) * EW);
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {
+                    const double2 kB = apply_pair<P>(W, lds2(zc + r * EW - 2), lds2(zc + r * EW + 2),
+                                                     col[r], col[r + 1], col[r + 3], col[r + 4], q[r]);
+                    const size_t gofs = size_t(r) * n;
+                    if (KB == K_A) {
+                        const double2 t0 = lds2(zs + C::Z_ELEMS + sT + r * TXO);
+                        const double2 t1 = lds2(zs + C::Z_ELEMS + C::T_ELEMS + sT + r * TXO);
+                        double2 v0, v1;
+                        v0.x = t0.x + (dt / 3.0) * kB.x;  v0.y = t0.y + (dt / 3.0) * kB.y;
+                        v1.x = t1.x + (dt / 2.0) * kB.x;  v1.y = t1.y + (dt / 2.0) * kB.y;
+                        *reinterpret_cast<double2 *>(o0 + gofs) = v0;
+                        *reinterpret_cast<double2 *>(o1 + gofs) = v1;
+                    } else {
+                        const double2 t0 = lds2(zs + C::Z_ELEMS + sT + r * TXO);
+                        double2 v0;
+                        v0.x = t0.x + (dt / 6.0) * kB.x;  v0.y = t0.y + (dt / 6.0) * kB.y;
+                        *reinterpret_cast<double2 *>(o0 + gofs) = v0;
+                    }
+                }
+            }
+            if (j >= 4) {
+                o0 += nn;
+                if (KB == K_A) o1 += nn;
+            }
+            if (j >= 2) {
+                mbar_arrive(&empty[zc_pos.slot]);
+                zc_pos.step(ZD);
+            }
+            zq_pos.step(ZD);
+        });
+        // release the item's last two Z planes (never a centre)
+        mbar_arrive(&empty[zc_pos.slot]);
+        zc_pos.step(ZD);
+        mbar_arrive(&empty[zc_pos.slot]);
+    }
+}
+
+template <int KB, class C>
+__global__ void __launch_bounds__(C::NT, 1)
+fused_persist_kernel(const StencilArgs a) {
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) uint64_t full[C::ZD], empty[C::ZD], in_full[C::DEPTH], in_empty[C::DEPTH];
+    const int items = a.tiles_x * a.tiles_y * a.chunks_z;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::ZD; ++s) {
+            mbar_init(&full[s], C::NTA);
+            mbar_init(&empty[s], C::NTB);
+        }
+        for (int s = 0; s < C::DEPTH; ++s) {
+            mbar_init(&in_full[s], 32);
+            mbar_init(&in_empty[s], C::NTA);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x < C::NTA)
+        stage_a_p<KB, C>(a, sm, items, full, empty, in_full, in_empty);
+    else if (threadIdx.x < C::NTA + C::NTB)
+        stage_b_p<KB, C>(a, sm, items, full, empty);
+    else
+        producer_p<KB, C>(a, sm, items, in_full, in_empty);
+}
+
 }  // namespace prk

@@ -220,9 +220,34 @@ static pr_status setup_fused_cfg(pr_grid *g) {
     return PR_OK;
 }
 
+template <int KB, class C>
+static pr_status setup_fused_persist(pr_grid *g) {
+    const size_t smem = C::template smem_bytes<KB>();
+    CK(cudaFuncSetAttribute(fused_persist_kernel<KB, C>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_persist_kernel<KB, C>, C::NT, smem));
+    if (occ < 1) return fail(PR_ECUDA, "persistent fused kernel %d cannot be resident", KB);
+    LaunchCfg &c = g->lf[KB];
+    const int n = g->n;
+    c.occ = occ;
+    c.threads = C::NT;
+    c.smem = smem;
+    c.tiles_x = n / C::TXO;
+    c.tiles_y = n / C::TYO;
+    const int slots = g->sms * occ;
+    const int ch = pick_chunks(n, c.tiles_x * c.tiles_y, slots, 4);
+    c.cz = (n + ch - 1) / ch;
+    c.chunks_z = (n + c.cz - 1) / c.cz;
+    const int items = c.tiles_x * c.tiles_y * c.chunks_z;
+    c.blocks = std::min(items, slots);  // persistent: one CTA per resident slot
+    return PR_OK;
+}
+
 template <int KB>
 static pr_status setup_fused(pr_grid *g) {
     switch (g->fvariant) {
+    case 10: return setup_fused_persist<KB, FusedP0>(g);
     case 1: return setup_fused_cfg<KB, Fused1>(g);
     case 2: return setup_fused_cfg<KB, Fused2>(g);
     case 3: return setup_fused_cfg<KB, Fused3>(g);
@@ -245,6 +270,7 @@ static void launch_fused(pr_grid *g, const StencilArgs &a0, cudaStream_t st) {
     a.cz = c.cz;
     a.chunks_z = c.chunks_z;
     switch (g->fvariant) {
+    case 10: fused_persist_kernel<KB, FusedP0><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     case 1: fused_kernel<KB, Fused1><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     case 2: fused_kernel<KB, Fused2><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     case 3: fused_kernel<KB, Fused3><<<c.blocks, c.threads, c.smem, st>>>(a); break;
@@ -706,7 +732,7 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
     if ((s = setup_kind<K_S4>(g)) != PR_OK) return bail(s);
     {
         const char *fe = getenv("PR_F2");
-        if (const char *fv = getenv("PR_FTILE")) g->fvariant = std::max(0, std::min(9, atoi(fv)));
+        if (const char *fv = getenv("PR_FTILE")) g->fvariant = std::max(0, std::min(10, atoi(fv)));
         g->f2 = (n % Fused0::TXO == 0) && (n % Fused0::TYO == 0) && !(fe && fe[0] == '0');
     }
     if (g->f2) {
