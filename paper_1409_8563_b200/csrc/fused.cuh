@@ -462,7 +462,7 @@ using Fused5 = FusedCfgX<32, 5, 3, 1, 4, 4>;
 using Fused6 = FusedCfgX<16, 6, 4, 1, 1, 2>;   // 12 stage-A warps : 4 stage-B warps
 using Fused7 = FusedCfgX<32, 6, 3, 1, 2, 4>;   // 32-row tile, 11 : 4
 using Fused8 = FusedCfgX<16, 6, 4, 1, 2, 2, 1>;   // Fused3 + producer warp
-using Fused9 = FusedCfgX<16, 7, 4, 1, 2, 2, 1>;   // same, deeper input ring (default, PR_FTILE=9)
+using Fused9 = FusedCfgX<16, 7, 4, 1, 2, 2, 1>;   // same, deeper input ring
 
 __device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
 __device__ __forceinline__ void sts2(double *p, double2 v) { *reinterpret_cast<double2 *>(p) = v; }
@@ -939,7 +939,7 @@ template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_> struct FusedCfgP 
                                  size_t(ZD) * ZS_ELEMS<KB>);
     }
 };
-using FusedP0 = FusedCfgP<16, 7, 4, 2, 2>;
+using FusedP0 = FusedCfgP<16, 7, 4, 2, 2>;   // default (PR_FTILE=10)
 
 struct WorkItem {
     int x0, y0, z_begin, nz;
