@@ -939,8 +939,8 @@ template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_> struct FusedCfgP 
                                  size_t(ZD) * ZS_ELEMS<KB>);
     }
 };
-using FusedP0 = FusedCfgP<16, 7, 4, 2, 2>;   // default (PR_FTILE=10)
-using FusedP1 = FusedCfgP<16, 9, 4, 2, 2>;   // deeper input ring
+using FusedP0 = FusedCfgP<16, 7, 4, 2, 2>;
+using FusedP1 = FusedCfgP<16, 9, 4, 2, 2>;   // deeper input ring (default, PR_FTILE=11)
 using FusedP2 = FusedCfgP<16, 9, 6, 2, 2>;   // deeper input and intermediate rings
 
 struct WorkItem {
