@@ -916,16 +916,16 @@ fused_kernel(const StencilArgs a) {
 // items, so the producer warp streams the next item's first planes while the
 // compute warps finish the current one (no per-item pipeline fill).  Aux planes
 // (K_B) share the slot index of the input element they ride with.
-template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_> struct FusedCfgP {
+template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_, int PW_ = 1> struct FusedCfgP {
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = 1, XP = 2,
-                         PROD = 1;
+                         PROD = 1, PW = PW_;  // PW producer warps
     static constexpr int RPTA = RPTA_, RPT = RPTB_;
     static constexpr int EW = TXO + 4, EH = TYO + 4, IW = TXO + 8, IH = TYO + 8;
     static constexpr int IWS = IW + 2, EWS = EW + 2;
     static constexpr int GA = EH / RPTA, GB = TYO / RPT;
     static constexpr int A_ITEMS = (EW / 2) * GA, B_ITEMS = (TXO / 2) * GB;
     static constexpr int WA = (A_ITEMS + 31) / 32, WB = (B_ITEMS + 31) / 32;
-    static constexpr int NTA = 32 * WA, NTB = 32 * WB, NTP = 32, NT = NTA + NTB + NTP;
+    static constexpr int NTA = 32 * WA, NTB = 32 * WB, NTP = 32 * PW, NT = NTA + NTB + NTP;
     static constexpr int AD = DEPTH;  // aux slots follow the input slots
     static constexpr int Y_ELEMS = IH * IWS, Z_ELEMS = EH * EWS, T_ELEMS = TYO * TXO;
     static constexpr int AUX_ELEMS = Z_ELEMS + T_ELEMS;
@@ -942,6 +942,7 @@ template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_> struct FusedCfgP 
 using FusedP0 = FusedCfgP<16, 7, 4, 2, 2>;
 using FusedP1 = FusedCfgP<16, 9, 4, 2, 2>;   // deeper input ring (default, PR_FTILE=11)
 using FusedP2 = FusedCfgP<16, 9, 6, 2, 2>;   // deeper input and intermediate rings
+using FusedP3 = FusedCfgP<16, 9, 4, 2, 2, 2>;   // two producer warps
 
 struct WorkItem {
     int x0, y0, z_begin, nz;
@@ -974,13 +975,14 @@ template <int KB, class C>
 __device__ __forceinline__ void producer_p(const StencilArgs &a, double *sm, int items,
                                            uint64_t *in_full, uint64_t *in_empty) {
     constexpr int DEPTH = C::DEPTH, EW = C::EWS, IW = C::IWS, TXO = C::TXO;
-    constexpr int NY = (C::Y_CHUNKS + 31) / 32, NU = (C::U_CHUNKS + 31) / 32,
-                  NC = (C::C_CHUNKS + 31) / 32;
+    constexpr int NP = C::NTP;
+    constexpr int NY = (C::Y_CHUNKS + NP - 1) / NP, NU = (C::U_CHUNKS + NP - 1) / NP,
+                  NC = (C::C_CHUNKS + NP - 1) / NP;
     double *yring = sm;
     double *aring = yring + size_t(DEPTH) * C::Y_ELEMS;
     const int n = a.n;
     const size_t nn = size_t(n) * n;
-    const int lane = threadIdx.x % 32;
+    const int lane = threadIdx.x - (C::NTA + C::NTB);  // 0 .. NP-1
     const uint32_t yring_s = smem_u32(yring), aring_s = smem_u32(aring);
     RingPos pos;
 #pragma unroll 1
@@ -990,7 +992,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, double *sm, int
         int ysrc[NY], ydst[NY];
 #pragma unroll
         for (int k = 0; k < NY; ++k) {
-            const int c = lane + 32 * k;
+            const int c = lane + NP * k;
             ysrc[k] = -1;
             ydst[k] = 0;
             if (c < C::Y_CHUNKS) {
@@ -1004,7 +1006,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, double *sm, int
         if constexpr (KB == K_B) {
 #pragma unroll
             for (int k = 0; k < NU; ++k) {
-                const int c = lane + 32 * k;
+                const int c = lane + NP * k;
                 usrc[k] = -1;
                 udst[k] = 0;
                 if (c < C::U_CHUNKS) {
@@ -1015,7 +1017,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, double *sm, int
             }
 #pragma unroll
             for (int k = 0; k < NC; ++k) {
-                const int c = lane + 32 * k;
+                const int c = lane + NP * k;
                 csrc[k] = -1;
                 cdst[k] = 0;
                 if (c < C::C_CHUNKS) {
@@ -1264,7 +1266,7 @@ fused_persist_kernel(const StencilArgs a) {
             mbar_init(&empty[s], C::NTB);
         }
         for (int s = 0; s < C::DEPTH; ++s) {
-            mbar_init(&in_full[s], 32);
+            mbar_init(&in_full[s], C::NTP);
             mbar_init(&in_empty[s], C::NTA);
         }
         fence_mbar_init();

@@ -2,8 +2,10 @@
 import csv, subprocess, sys
 rep, which = sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 0
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                      "--launch-skip", str(which), "--launch-count", "1"],
                      capture_output=True, text=True).stdout
+which = 0
 rows = list(csv.reader(out.splitlines()))
 blocks, cur = [], None
 for r in rows:
