@@ -947,6 +947,11 @@ using FusedP3 = FusedCfgP<16, 9, 4, 2, 2, 2>;   // two producer warps
 struct WorkItem {
     int x0, y0, z_begin, nz;
 };
+// periodic wrap of an index known to lie in [-n, 2n) (fused path: n >= 32, halo <= 4)
+__device__ __forceinline__ int wrap1(int i, int n) {
+    i += (i < 0) ? n : 0;
+    return i - ((i >= n) ? n : 0);
+}
 __device__ __forceinline__ WorkItem decode_item(const StencilArgs &a, int item, int txo, int tyo) {
     WorkItem w;
     int b = item;
@@ -982,7 +987,8 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, double *sm, int
     double *aring = yring + size_t(DEPTH) * C::Y_ELEMS;
     const int n = a.n;
     const size_t nn = size_t(n) * n;
-    const int lane = threadIdx.x - (C::NTA + C::NTB);  // 0 .. NP-1
+    // 0 .. NP-1 (NTA + NTB is a multiple of 32, so the % keeps the range visible)
+    const int lane = (threadIdx.x - (C::NTA + C::NTB)) % NP;
     const uint32_t yring_s = smem_u32(yring), aring_s = smem_u32(aring);
     RingPos pos;
 #pragma unroll 1
@@ -997,7 +1003,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, double *sm, int
             ydst[k] = 0;
             if (c < C::Y_CHUNKS) {
                 const int r = c / (C::IW / 2), cc = c % (C::IW / 2);
-                ysrc[k] = wrapi(w.y0 - 4 + r, n) * n + wrapi(w.x0 - 4 + 2 * cc, n);
+                ysrc[k] = wrap1(w.y0 - 4 + r, n) * n + wrap1(w.x0 - 4 + 2 * cc, n);
                 ydst[k] = 8 * (r * IW + 2 * cc);
             }
         }
@@ -1011,7 +1017,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, double *sm, int
                 udst[k] = 0;
                 if (c < C::U_CHUNKS) {
                     const int r = c / (C::EW / 2), cc = c % (C::EW / 2);
-                    usrc[k] = wrapi(w.y0 - 2 + r, n) * n + wrapi(w.x0 - 2 + 2 * cc, n);
+                    usrc[k] = wrap1(w.y0 - 2 + r, n) * n + wrap1(w.x0 - 2 + 2 * cc, n);
                     udst[k] = 8 * (r * EW + 2 * cc);
                 }
             }
@@ -1027,7 +1033,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, double *sm, int
                 }
             }
         }
-        int zin = wrapi(w.z_begin - 4, n);
+        int zin = wrap1(w.z_begin - 4, n);
 #pragma unroll 1
         for (int e = 0; e < E; ++e) {
             if (pos.round > 0) mbar_wait(&in_empty[pos.slot], (pos.round - 1) & 1);
