@@ -943,6 +943,7 @@ using FusedP0 = FusedCfgP<16, 7, 4, 2, 2>;
 using FusedP1 = FusedCfgP<16, 9, 4, 2, 2>;   // deeper input ring (default, PR_FTILE=11)
 using FusedP2 = FusedCfgP<16, 9, 6, 2, 2>;   // deeper input and intermediate rings
 using FusedP3 = FusedCfgP<16, 9, 4, 2, 2, 2>;   // two producer warps
+using FusedP4 = FusedCfgP<16, 9, 4, 2, 2, 3>;   // three producer warps
 
 struct WorkItem {
     int x0, y0, z_begin, nz;
