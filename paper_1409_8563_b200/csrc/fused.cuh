@@ -940,9 +940,9 @@ template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_, int PW_ = 1> stru
     }
 };
 using FusedP0 = FusedCfgP<16, 7, 4, 2, 2>;
-using FusedP1 = FusedCfgP<16, 9, 4, 2, 2>;   // deeper input ring (default, PR_FTILE=11)
+using FusedP1 = FusedCfgP<16, 9, 4, 2, 2>;   // deeper input ring
 using FusedP2 = FusedCfgP<16, 9, 6, 2, 2>;   // deeper input and intermediate rings
-using FusedP3 = FusedCfgP<16, 9, 4, 2, 2, 2>;   // two producer warps
+using FusedP3 = FusedCfgP<16, 9, 4, 2, 2, 2>;   // two producer warps (default, PR_FTILE=13)
 using FusedP4 = FusedCfgP<16, 9, 4, 2, 2, 3>;   // three producer warps
 
 struct WorkItem {

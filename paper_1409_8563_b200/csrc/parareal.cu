@@ -86,7 +86,7 @@ struct pr_grid {
     int dev = 0;
     int variant = 0;                    // stencil tile variant (PR_TILE env, tuning)
     bool f2 = false;                    // fused two-kernel RK4 step (tile-aligned n)
-    int fvariant = 11;                  // fused tile variant (PR_FTILE env, tuning)
+    int fvariant = 13;                  // fused tile variant (PR_FTILE env, tuning)
     LaunchCfg lf[2];                    // launch configs of fused_kernel<K_A>, <K_B>
     pr_problem prob{};
     int n = 0;
