@@ -340,6 +340,11 @@ def main():
             defects = d
     barrier()
     q1 = energy.read_j()
+    tl_all = [None] * world
+    if world > 1:
+        dist.all_gather_object(tl_all, pr.pr_last_timings(grid))
+    else:
+        tl_all = [pr.pr_last_timings(grid)]
     Q_p_rank = (q1 - q0) / args.steps if (q0 is not None and q1 is not None) else float("nan")
     Q_p = sum_over_ranks(Q_p_rank)
     Q_s = max_over_ranks(Q_s if Q_s is not None else float("nan"))
@@ -429,6 +434,7 @@ def main():
                         "C_f_ms": C_f_ms, "C_p_ms": ms_per_step, "tau_f_ms": tf_all,
                         "tau_c_ms": tc_all, "tau_c_over_tau_f": r, "N_c_over_N_f": nc / nf,
                         "defects": dlist, "tol": args.tol,
+                        "rank_timings_ms": tl_all,
                         "iterations_run": pr.pr_last_monitors(grid)[1],
                         "iterate_change_monitor": pr.pr_last_monitors(grid)[0]},
             "energy": {"Q_serial_J": Q_s, "Q_parareal_J": Q_p,
