@@ -944,6 +944,8 @@ using FusedP1 = FusedCfgP<16, 9, 4, 2, 2>;   // deeper input ring
 using FusedP2 = FusedCfgP<16, 9, 6, 2, 2>;   // deeper input and intermediate rings
 using FusedP3 = FusedCfgP<16, 9, 4, 2, 2, 2>;   // two producer warps (default, PR_FTILE=13)
 using FusedP4 = FusedCfgP<16, 9, 4, 2, 2, 3>;   // three producer warps
+using FusedP5 = FusedCfgP<16, 9, 6, 2, 2, 2>;   // two producers, 6-slot intermediate ring
+using FusedP6 = FusedCfgP<16, 8, 5, 2, 2, 2>;   // two producers, 8 / 5 slots
 
 struct WorkItem {
     int x0, y0, z_begin, nz;

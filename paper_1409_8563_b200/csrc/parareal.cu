@@ -252,6 +252,8 @@ static pr_status setup_fused(pr_grid *g) {
     case 12: return setup_fused_persist<KB, FusedP2>(g);
     case 13: return setup_fused_persist<KB, FusedP3>(g);
     case 14: return setup_fused_persist<KB, FusedP4>(g);
+    case 15: return setup_fused_persist<KB, FusedP5>(g);
+    case 16: return setup_fused_persist<KB, FusedP6>(g);
     case 1: return setup_fused_cfg<KB, Fused1>(g);
     case 2: return setup_fused_cfg<KB, Fused2>(g);
     case 3: return setup_fused_cfg<KB, Fused3>(g);
@@ -279,6 +281,8 @@ static void launch_fused(pr_grid *g, const StencilArgs &a0, cudaStream_t st) {
     case 12: fused_persist_kernel<KB, FusedP2><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     case 13: fused_persist_kernel<KB, FusedP3><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     case 14: fused_persist_kernel<KB, FusedP4><<<c.blocks, c.threads, c.smem, st>>>(a); break;
+    case 15: fused_persist_kernel<KB, FusedP5><<<c.blocks, c.threads, c.smem, st>>>(a); break;
+    case 16: fused_persist_kernel<KB, FusedP6><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     case 1: fused_kernel<KB, Fused1><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     case 2: fused_kernel<KB, Fused2><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     case 3: fused_kernel<KB, Fused3><<<c.blocks, c.threads, c.smem, st>>>(a); break;
@@ -740,7 +744,7 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
     if ((s = setup_kind<K_S4>(g)) != PR_OK) return bail(s);
     {
         const char *fe = getenv("PR_F2");
-        if (const char *fv = getenv("PR_FTILE")) g->fvariant = std::max(0, std::min(14, atoi(fv)));
+        if (const char *fv = getenv("PR_FTILE")) g->fvariant = std::max(0, std::min(16, atoi(fv)));
         g->f2 = (n % Fused0::TXO == 0) && (n % Fused0::TYO == 0) && !(fe && fe[0] == '0');
     }
     if (g->f2) {
