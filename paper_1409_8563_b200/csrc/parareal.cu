@@ -4,6 +4,7 @@
 //
 // Nothing here includes or calls the CPU oracle (oracle/); this file and
 // kernels.cuh are the whole product path.
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -86,8 +87,8 @@ struct pr_grid {
     int dev = 0;
     int variant = 0;                    // stencil tile variant (PR_TILE env, tuning)
     bool f2 = false;                    // fused two-kernel RK4 step (tile-aligned n)
-    int fvariant = 13;                  // fused tile variant (PR_FTILE env, tuning)
-    LaunchCfg lf[2];                    // launch configs of fused_kernel<K_A>, <K_B>
+    int fvariant = 14;                  // fused tile variant (PR_FTILE env 10..19, tuning)
+    LaunchCfg lf[2];                    // launch configs of fused_persist_kernel<K_A>, <K_B>
     pr_problem prob{};
     int n = 0;
     int64_t N = 0;
@@ -120,7 +121,35 @@ struct pr_grid {
     std::vector<double> monitors;           // iterate-change monitor of the last pr_parareal
     int iters = 0;                          // iterations it ran
     double *h_flag = nullptr;               // pinned: received stop flag
+    pr_status launch_err = PR_OK;           // sticky error of an enqueue helper (TMA map encode)
 };
+
+// ------------------------------------------------------------------ TMA tensor maps
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// 3-D map of an n^3 fp64 field (x fastest), box bx x by x 1 (one z plane of a tile)
+static bool tma_encode3(CUtensorMap *m, const double *p, int n, int bx, int by) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tma_encoder();
+    if (!enc || !p) return false;
+    const cuuint64_t dims[3] = {cuuint64_t(n), cuuint64_t(n), cuuint64_t(n)};
+    const cuuint64_t strides[2] = {cuuint64_t(n) * 8, cuuint64_t(n) * n * 8};
+    const cuuint32_t box[3] = {cuuint32_t(bx), cuuint32_t(by), 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(p), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 template <int KIND, class C>
 static pr_status setup_kind_cfg(pr_grid *g) {
@@ -199,35 +228,20 @@ static int pick_chunks(int n, int tiles, int slots, int halo) {
 }
 
 template <int KB, class C>
-static pr_status setup_fused_cfg(pr_grid *g) {
-    const size_t smem = C::template smem_bytes<KB>();
-    CK(cudaFuncSetAttribute(fused_kernel<KB, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(smem)));
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel<KB, C>, C::NT, smem));
-    if (occ < 1) return fail(PR_ECUDA, "fused kernel %d cannot be resident", KB);
-    LaunchCfg &c = g->lf[KB];
-    const int n = g->n;
-    c.occ = occ;
-    c.threads = C::NT;
-    c.smem = smem;
-    c.tiles_x = n / C::TXO;
-    c.tiles_y = n / C::TYO;
-    const int ch = pick_chunks(n, c.tiles_x * c.tiles_y, g->sms * occ, 4);
-    c.cz = (n + ch - 1) / ch;
-    c.chunks_z = (n + c.cz - 1) / c.cz;
-    c.blocks = c.tiles_x * c.tiles_y * c.chunks_z;
-    return PR_OK;
-}
-
-template <int KB, class C>
 static pr_status setup_fused_persist(pr_grid *g) {
     const size_t smem = C::template smem_bytes<KB>();
     CK(cudaFuncSetAttribute(fused_persist_kernel<KB, C>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_persist_kernel<KB, C>, C::NT, smem));
-    if (occ < 1) return fail(PR_ECUDA, "persistent fused kernel %d cannot be resident", KB);
+    if (occ < 1) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, fused_persist_kernel<KB, C>);
+        return fail(PR_ECUDA,
+                    "persistent fused kernel %d cannot be resident (%d threads, %d regs, %zu B smem, "
+                    "max threads %d)",
+                    KB, C::NT, fa.numRegs, smem, fa.maxThreadsPerBlock);
+    }
     LaunchCfg &c = g->lf[KB];
     const int n = g->n;
     c.occ = occ;
@@ -254,17 +268,29 @@ static pr_status setup_fused(pr_grid *g) {
     case 14: return setup_fused_persist<KB, FusedP4>(g);
     case 15: return setup_fused_persist<KB, FusedP5>(g);
     case 16: return setup_fused_persist<KB, FusedP6>(g);
-    case 1: return setup_fused_cfg<KB, Fused1>(g);
-    case 2: return setup_fused_cfg<KB, Fused2>(g);
-    case 3: return setup_fused_cfg<KB, Fused3>(g);
-    case 4: return setup_fused_cfg<KB, Fused4>(g);
-    case 5: return setup_fused_cfg<KB, Fused5>(g);
-    case 6: return setup_fused_cfg<KB, Fused6>(g);
-    case 7: return setup_fused_cfg<KB, Fused7>(g);
-    case 8: return setup_fused_cfg<KB, Fused8>(g);
-    case 9: return setup_fused_cfg<KB, Fused9>(g);
-    default: return setup_fused_cfg<KB, Fused0>(g);
+    case 17: return setup_fused_persist<KB, FusedP7>(g);
+    case 18: return setup_fused_persist<KB, FusedP8>(g);
+    case 19: return setup_fused_persist<KB, FusedP9>(g);
+    default: return setup_fused_persist<KB, FusedP4>(g);
     }
+}
+
+template <int KB, class C>
+static void launch_persist(pr_grid *g, const StencilArgs &a, const LaunchCfg &c, cudaStream_t st) {
+    TmaMaps tm;
+    memset(&tm, 0, sizeof tm);
+    if constexpr (C::FILL == 2) {
+        bool ok = tma_encode3(&tm.y, a.y, g->n, C::IWS, C::IH);
+        if (KB == K_B) {
+            ok = ok && tma_encode3(&tm.u, a.p0, g->n, C::EWS, C::EH);
+            ok = ok && tma_encode3(&tm.c, a.p1, g->n, C::TXO, C::TYO);
+        }
+        if (!ok) {
+            g->launch_err = fail(PR_ECUDA, "cuTensorMapEncodeTiled failed (fused kernel %d)", KB);
+            return;
+        }
+    }
+    fused_persist_kernel<KB, C><<<c.blocks, c.threads, c.smem, st>>>(a, tm);
 }
 
 template <int KB>
@@ -276,23 +302,17 @@ static void launch_fused(pr_grid *g, const StencilArgs &a0, cudaStream_t st) {
     a.cz = c.cz;
     a.chunks_z = c.chunks_z;
     switch (g->fvariant) {
-    case 10: fused_persist_kernel<KB, FusedP0><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 11: fused_persist_kernel<KB, FusedP1><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 12: fused_persist_kernel<KB, FusedP2><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 13: fused_persist_kernel<KB, FusedP3><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 14: fused_persist_kernel<KB, FusedP4><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 15: fused_persist_kernel<KB, FusedP5><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 16: fused_persist_kernel<KB, FusedP6><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 1: fused_kernel<KB, Fused1><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 2: fused_kernel<KB, Fused2><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 3: fused_kernel<KB, Fused3><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 4: fused_kernel<KB, Fused4><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 5: fused_kernel<KB, Fused5><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 6: fused_kernel<KB, Fused6><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 7: fused_kernel<KB, Fused7><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 8: fused_kernel<KB, Fused8><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    case 9: fused_kernel<KB, Fused9><<<c.blocks, c.threads, c.smem, st>>>(a); break;
-    default: fused_kernel<KB, Fused0><<<c.blocks, c.threads, c.smem, st>>>(a); break;
+    case 10: launch_persist<KB, FusedP0>(g, a, c, st); break;
+    case 11: launch_persist<KB, FusedP1>(g, a, c, st); break;
+    case 12: launch_persist<KB, FusedP2>(g, a, c, st); break;
+    case 13: launch_persist<KB, FusedP3>(g, a, c, st); break;
+    case 14: launch_persist<KB, FusedP4>(g, a, c, st); break;
+    case 15: launch_persist<KB, FusedP5>(g, a, c, st); break;
+    case 16: launch_persist<KB, FusedP6>(g, a, c, st); break;
+    case 17: launch_persist<KB, FusedP7>(g, a, c, st); break;
+    case 18: launch_persist<KB, FusedP8>(g, a, c, st); break;
+    case 19: launch_persist<KB, FusedP9>(g, a, c, st); break;
+    default: launch_persist<KB, FusedP4>(g, a, c, st); break;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -543,6 +563,11 @@ static pr_status run_fine2(pr_grid *g, const double *uin, double *uout, int64_t 
     }
     (void)state;
     CKL();
+    if (g->launch_err != PR_OK) {
+        const pr_status e = g->launch_err;
+        g->launch_err = PR_OK;
+        return e;
+    }
     return PR_OK;
 }
 
@@ -744,8 +769,8 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
     if ((s = setup_kind<K_S4>(g)) != PR_OK) return bail(s);
     {
         const char *fe = getenv("PR_F2");
-        if (const char *fv = getenv("PR_FTILE")) g->fvariant = std::max(0, std::min(16, atoi(fv)));
-        g->f2 = (n % Fused0::TXO == 0) && (n % Fused0::TYO == 0) && !(fe && fe[0] == '0');
+        if (const char *fv = getenv("PR_FTILE")) g->fvariant = std::max(10, std::min(19, atoi(fv)));
+        g->f2 = (n % FusedP4::TXO == 0) && (n % FusedP4::TYO == 0) && !(fe && fe[0] == '0');
     }
     if (g->f2) {
         if ((s = setup_fused<K_A>(g)) != PR_OK) return bail(s);

@@ -234,6 +234,28 @@ def test_fine_paths_agree(n, f2, monkeypatch):
     g.destroy()
 
 
+@pytest.mark.parametrize("variant", [str(v) for v in range(10, 20)])
+def test_fused_variants_bitwise(variant, monkeypatch):
+    """Every persistent fused tile variant (PR_FTILE) gives the four-stage
+    path's bits: same folded weights, same operation order per point.  n = 128
+    has tiles on and away from the periodic seams (cp.async and TMA fills)."""
+    n = 128
+    u0 = dev(random_field(n, 31))
+    outs = []
+    for f2, v in (("0", "13"), ("1", variant)):
+        monkeypatch.setenv("PR_F2", f2)
+        monkeypatch.setenv("PR_FTILE", v)
+        try:
+            g = pr.Grid(pr.Problem(n, c=PARITY_C))
+        except pr.PrError as e:  # a tuning variant that does not fit this GPU
+            pytest.skip(str(e))
+        out = torch.empty_like(u0)
+        pr.pr_fine(g, u0, out, 3, 21, 1e-4)
+        outs.append(out)
+        g.destroy()
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("n", [128, 256])
 def test_full_size_steps_vs_oracle(n):
     """Launch configuration bench.py times, a few steps, all n^3 outputs."""

@@ -25,7 +25,11 @@ for ch in chunks:
             os.environ.pop("PR_CHUNKS_Z", None)
         else:
             os.environ["PR_CHUNKS_Z"] = ch
-        g = pr.Grid(pr.Problem(n), 0)
+        try:
+            g = pr.Grid(pr.Problem(n), 0)
+        except pr.PrError as e:
+            print(f"n={n} variant={v}: {e}", flush=True)
+            continue
         if u0 is None:
             u0 = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
             pr.pr_fill_sine(g, u0)
