@@ -1,6 +1,6 @@
 """Turn gpurun_out ncu outputs into the committed profiles/ summaries.
 
-    python tools/make_profiles.py <round> <launches.csv> <full.ncu-rep> [n]
+    python tools/make_profiles.py <round> <launches.csv> <full.ncu-rep> [n] [tag]
 Writes profiles/r<round>_launch_shares_cfg3p.txt, r<round>_launches_cfg3p.csv,
 r<round>_ncu_full_k<n>_summary.txt and updates profiles/ncu_summary.json
 (dram bytes per RK4 step for the fused and four-stage paths)."""
@@ -14,6 +14,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rnd, launches, rep = sys.argv[1], sys.argv[2], sys.argv[3]
 n = int(sys.argv[4]) if len(sys.argv) > 4 else 256
+tag = sys.argv[5] + "_" if len(sys.argv) > 5 else ""
 P = os.path.join(ROOT, "profiles")
 
 rows = list(csv.reader(open(launches)))
@@ -47,7 +48,7 @@ with open(os.path.join(P, f"r{rnd}_launches_cfg3p.csv"), "w") as f:
 
 out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep],
                      capture_output=True, text=True).stdout
-open(os.path.join(P, f"r{rnd}_ncu_full_k{n}_summary.txt"), "w").write(out)
+open(os.path.join(P, f"r{rnd}_ncu_full_{tag}k{n}_summary.txt"), "w").write(out)
 
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(raw.splitlines()))
@@ -58,7 +59,7 @@ for row in r[2:]:
     b = sum(float(row[h.index(m)]) * scale[units[h.index(m)]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     per[row[h.index("Kernel Name")]].append((b, float(row[h.index("gpu__time_duration.sum")])))
 avg = {k: [sum(x[0] for x in v) / len(v), sum(x[1] for x in v) / len(v)] for k, v in per.items()}
-fused = sum(b for k, (b, t) in avg.items() if "fused_kernel" in k)
+fused = sum(b for k, (b, t) in avg.items() if "fused_" in k)
 four = sum(b for k, (b, t) in avg.items() if any(f"stencil_kernel<{i}," in k for i in (1, 2, 3, 4)))
 p = os.path.join(P, "ncu_summary.json")
 js = json.load(open(p)) if os.path.exists(p) else {}
@@ -70,7 +71,7 @@ if fused:
 if four:
     js["fine_step_dram_bytes"].setdefault("four_stage", {})[str(n)] = four
     js["fine_step_algorithmic_bytes"].setdefault("four_stage", {})[str(n)] = 128 * n ** 3
-js["per_launch_bytes_and_us"] = avg
+js.setdefault("per_launch_bytes_and_us", {}).update(avg)
 js["note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch (bytes) and gpu__time_duration (us) "
               f"from ncu --set full --clock-control none, round {rnd}, tools/profile_kernels.py {n}")
 json.dump(js, open(p, "w"), indent=1)
