@@ -224,6 +224,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--K", type=int, default=None, help="override K (default min(3, N_p))")
     ap.add_argument("--slices", type=int, default=None, help="override N_p (default = world size)")
+    ap.add_argument("--handoff", default="peer", choices=["nccl", "peer"],
+                    help="hand-off of u^{k+1} between ranks: ncclSend/Recv or peer stores "
+                         "from the correction kernel (PR_FLAG_PEER_HANDOFF)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--nu-mode", type=int, default=None)
@@ -313,7 +316,8 @@ def main():
     tc_all = max_over_ranks(tau_c)
     C_f_ms = max_over_ranks(C_f_ms)
 
-    pcfg = pr.PararealCfg(Np, nc, nf, K, tol=args.tol)
+    pcfg = pr.PararealCfg(Np, nc, nf, K, tol=args.tol,
+                          flags=pr.PR_FLAG_PEER_HANDOFF if args.handoff == "peer" else 0)
     for _ in range(args.warmup):
         pr.pr_parareal(grid, pcfg, u0, uT if last else None, uref)
     barrier()
@@ -426,6 +430,7 @@ def main():
                        "omega": cfg.omega, "nu_mode": ["stage", "step_start"][cfg.nu_mode],
                        "c": list(cfg.c), "parallelism": f"time-parallel Parareal, {world} GPU(s), "
                                                         f"{Np // world} slice(s)/GPU",
+                       "handoff": args.handoff if world > 1 else "none",
                        "l2": "inputs larger than L2 (128 MiB fields at 256^3)" if n >= 256 else
                              "fields L2-resident"},
             "speedup": {"S_measured": S_meas, "S_bound_eq_speedup_P229": S_bound,

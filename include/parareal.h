@@ -80,11 +80,13 @@ typedef struct {
     int32_t n_coarse_per_slice;  /* N_c >= 1, Delta t = T / (N_p N_c) */
     int32_t n_fine_per_slice;    /* N_f >= 1, delta t = T / (N_p N_f) */
     int32_t K;                   /* iterations k_max >= 0 (K = 0: coarse guess only) */
-    int32_t flags;               /* bit 0 (PR_FLAG_G_IS_F): use F for G (degenerate test) */
+    int32_t flags;               /* bit 0 (PR_FLAG_G_IS_F): use F for G (degenerate test);
+                                    bit 1 (PR_FLAG_PEER_HANDOFF): hand-off by peer stores (below) */
     double tol;                  /* > 0: convergence-controlled stopping (below); <= 0: fixed K */
 } pr_parareal_cfg;
 
 #define PR_FLAG_G_IS_F 1
+#define PR_FLAG_PEER_HANDOFF 2
 
 typedef struct pr_grid pr_grid;  /* opaque */
 
@@ -152,6 +154,16 @@ pr_status pr_comm_init(pr_grid *grid, int32_t world, int32_t rank, const void *n
  * c_k <= tol, or when k = K-1; the stop flag rides on its last hand-off
  * message.  Iterations not run leave NaN in defects_host.  The monitors and
  * the iteration count are returned by pr_last_monitors.
+ * Hand-off: ncclSend / ncclRecv of u^{k+1} on a comm stream by
+ * default.  With PR_FLAG_PEER_HANDOFF (same value on every rank; world > 1; the
+ * GPUs of one node with peer access) the correction pass of a rank's last
+ * slice also stores u^{k+1} straight into the successor's receive buffer over
+ * NVLink (CUDA IPC mappings, exchanged once per buffer pool by an NCCL
+ * all-gather), a one-thread kernel then publishes a sequence word in the
+ * successor's memory with a system-scope release, and the successor's stream
+ * waits on that word (cuStreamWaitValue32: the stream front end waits, no
+ * kernel spins); the successor hands its receive buffer back the same way
+ * after the F that last reads it.  Results are bitwise those of the NCCL path.
  * Errors: PR_EINVAL, PR_ESTATE (world > 1 without a communicator), PR_ENCCL,
  * PR_EDOMAIN (u_ref all zero), PR_ECUDA. */
 pr_status pr_parareal(pr_grid *grid, const pr_parareal_cfg *cfg, const double *u0,

@@ -15,14 +15,14 @@ import ctypes
 from dataclasses import dataclass
 
 from . import _lib
-from ._lib import (PR_NU_STAGE, PR_NU_STEP_START, PR_FLAG_G_IS_F, PrError, OPS,
+from ._lib import (PR_NU_STAGE, PR_NU_STEP_START, PR_FLAG_G_IS_F, PR_FLAG_PEER_HANDOFF, PrError, OPS,
                    PR_NCCL_ID_BYTES)
 
 __all__ = ["Problem", "PararealCfg", "Grid", "pr_create_grid", "pr_destroy_grid", "pr_fine",
            "pr_coarse", "pr_defect", "pr_fill_sine", "pr_correct", "pr_nccl_unique_id",
            "pr_comm_init", "pr_parareal", "pr_plan", "pr_last_timings", "pr_kernel_launches",
            "pr_stability_ratio", "pr_last_error", "pr_version", "pr_grid_info", "pr_last_monitors", "PrError", "PR_NU_STAGE",
-           "PR_NU_STEP_START", "PR_FLAG_G_IS_F", "comm_init_torch"]
+           "PR_NU_STEP_START", "PR_FLAG_G_IS_F", "PR_FLAG_PEER_HANDOFF", "comm_init_torch"]
 
 
 @dataclass

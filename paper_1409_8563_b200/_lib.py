@@ -17,6 +17,7 @@ STATUS_NAMES = {0: "PR_OK", 1: "PR_EINVAL", 2: "PR_ENOMEM", 3: "PR_ECUDA", 4: "P
                 5: "PR_EDOMAIN", 6: "PR_ESTATE"}
 PR_NU_STAGE, PR_NU_STEP_START = 0, 1
 PR_FLAG_G_IS_F = 1
+PR_FLAG_PEER_HANDOFF = 2
 PR_NCCL_ID_BYTES = 128
 OPS = {1: "G_PREFIX", 2: "G_INIT", 3: "DEFECT0", 4: "F", 5: "RECV", 6: "G", 7: "CORRECT",
        8: "SEND", 9: "END_ITER"}

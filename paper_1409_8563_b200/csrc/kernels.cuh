@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(RED_THREADS)
 correct_kernel(const double2 *__restrict__ f, const double2 *__restrict__ gn,
                const double2 *__restrict__ go, double2 *uo, const double2 *__restrict__ ref,
                unsigned long long *dmax, const double2 *prev, unsigned long long *cmax,
-               unsigned long long *nmax, long long n2) {
+               unsigned long long *nmax, long long n2, double2 *peer) {
     unsigned long long m = 0, mc = 0, mn = 0;
     for (long long i = blockIdx.x * (long long)RED_THREADS + threadIdx.x; i < n2;
          i += (long long)gridDim.x * RED_THREADS) {
@@ -401,6 +401,7 @@ correct_kernel(const double2 *__restrict__ f, const double2 *__restrict__ gn,
             mn = umax64(mn, umax64(abs_bits(v.x), abs_bits(v.y)));
         }
         uo[i] = v;
+        if (peer) peer[i] = v;  // hand-off: the successor's receive buffer over NVLink (R7)
         if (ref) {
             const double2 r = __ldcs(ref + i);
             m = umax64(m, umax64(abs_bits(v.x - r.x), abs_bits(v.y - r.y)));
@@ -417,6 +418,16 @@ correct_kernel(const double2 *__restrict__ f, const double2 *__restrict__ gn,
 
 // set the stop-flag element that trails a hand-off buffer (C23)
 __global__ void set_flag_kernel(double *p, double v) { *p = v; }
+
+// Peer hand-off publication (one thread): optional stop flag into the peer's
+// message tail, then the sequence word with system-scope release semantics, so
+// every store of the preceding kernels in this stream (the correction's peer
+// stores) is visible to the device that observes `seq`.
+__global__ void post_kernel(double *stop_dst, double stop, unsigned int *flag, unsigned int seq) {
+    if (stop_dst) *stop_dst = stop;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(seq) : "memory");
+}
 
 // *d_diff = max|u - ref| (if u and d_diff), *d_ref = max|ref| (if d_ref)
 __global__ void __launch_bounds__(RED_THREADS)

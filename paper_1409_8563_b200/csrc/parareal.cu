@@ -122,7 +122,31 @@ struct pr_grid {
     int iters = 0;                          // iterations it ran
     double *h_flag = nullptr;               // pinned: received stop flag
     pr_status launch_err = PR_OK;           // sticky error of an enqueue helper (TMA map encode)
+    // peer hand-off (PR_FLAG_PEER_HANDOFF): flag words [0] data sequence (written by the
+    // predecessor), [1] free sequence (written by the successor); IPC mappings of the
+    // successor's two receive buffers and flag words and of the predecessor's flag words
+    unsigned int *d_flags = nullptr;
+    unsigned char *d_ipc = nullptr;         // all-gather staging of the IPC handles
+    double *peer_mail[2] = {nullptr, nullptr};
+    unsigned int *succ_flags = nullptr, *pred_flags = nullptr;
+    std::vector<void *> ipc_open;
+    long long pool_gen = 0, mapped_gen = -1;
+    unsigned int seq_base = 0;              // advances by K + 2 per peer-mode pr_parareal
 };
+
+// cuStreamWaitValue32 through the runtime's driver entry point: the stream's
+// front end waits on a 32-bit word (no kernel spins).
+static PFN_cuStreamWaitValue32_v11070 stream_wait_fn() {
+    static PFN_cuStreamWaitValue32_v11070 fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
+    }();
+    return fn;
+}
 
 // ------------------------------------------------------------------ TMA tensor maps
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
@@ -794,6 +818,8 @@ pr_status pr_destroy_grid(pr_grid *g) {
     cudaDeviceSynchronize();
     for (auto &kv : g->graphs) cudaGraphExecDestroy(kv.second.first);
     g->graphs.clear();
+    for (void *p : g->ipc_open) cudaIpcCloseMemHandle(p);
+    cudaFree(g->d_flags); cudaFree(g->d_ipc);
     if (g->comm) ncclCommDestroy(g->comm);
     for (double *p : g->pool) cudaFree(p);
     cudaFree(g->acc); cudaFree(g->ya); cudaFree(g->yb); cudaFree(g->ctmp);
@@ -905,12 +931,12 @@ static pr_status launch_correct(pr_grid *g, const double *f, const double *gn, c
                                 double *uo, const double *ref, unsigned long long *dmax,
                                 cudaStream_t st, const double *prev = nullptr,
                                 unsigned long long *cmax = nullptr,
-                                unsigned long long *nmax = nullptr) {
+                                unsigned long long *nmax = nullptr, double *peer = nullptr) {
     correct_kernel<<<red_blocks(g), RED_THREADS, 0, st>>>(
         reinterpret_cast<const double2 *>(f), reinterpret_cast<const double2 *>(gn),
         reinterpret_cast<const double2 *>(go), reinterpret_cast<double2 *>(uo),
         reinterpret_cast<const double2 *>(ref), dmax, reinterpret_cast<const double2 *>(prev),
-        cmax, nmax, g->N / 2);
+        cmax, nmax, g->N / 2, reinterpret_cast<double2 *>(peer));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     CKL();
     return PR_OK;
@@ -1067,6 +1093,75 @@ static pr_status wait_all(pr_grid *g, cudaStream_t st, int k_hint, bool with_com
                         ncclGetErrorString(r_));                                         \
     } while (0)
 
+// Peer hand-off setup, collective over the communicator, once per buffer pool:
+// every rank exports (CUDA IPC) the two pool fields that alternate as its
+// receive buffer and its flag words; the handles travel by one ncclAllGather;
+// rank r maps its successor's buffers and flags and its predecessor's flags.
+static pr_status peer_setup(pr_grid *g, double *mail_even, double *mail_odd) {
+    if (g->mapped_gen == g->pool_gen) return PR_OK;
+    for (void *p : g->ipc_open) cudaIpcCloseMemHandle(p);
+    g->ipc_open.clear();
+    g->peer_mail[0] = g->peer_mail[1] = nullptr;
+    g->succ_flags = g->pred_flags = nullptr;
+    g->mapped_gen = -1;
+    if (!stream_wait_fn()) return fail(PR_ECUDA, "cuStreamWaitValue32 entry point not found");
+    const int W = g->world, r = g->rank;
+    constexpr size_t REC = 3 * sizeof(cudaIpcMemHandle_t);
+    // flag words are zeroed once and never reset: sequence numbers only grow
+    // (seq_base advances on every peer-mode call, on every rank alike), so a late
+    // store from a peer's previous call can never satisfy a newer wait
+    if (!g->d_flags) {
+        CK(cudaMalloc(&g->d_flags, 256));
+        CK(cudaMemset(g->d_flags, 0, 256));
+    }
+    if (g->d_ipc) CK(cudaFree(g->d_ipc));
+    g->d_ipc = nullptr;
+    CK(cudaMalloc(&g->d_ipc, REC * size_t(W)));
+    cudaIpcMemHandle_t h[3];
+    CK(cudaIpcGetMemHandle(&h[0], mail_even));
+    CK(cudaIpcGetMemHandle(&h[1], mail_odd));
+    CK(cudaIpcGetMemHandle(&h[2], g->d_flags));
+    CK(cudaMemcpy(g->d_ipc + REC * size_t(r), h, REC, cudaMemcpyHostToDevice));
+    NCK(ncclAllGather(g->d_ipc + REC * size_t(r), g->d_ipc, REC, ncclUint8, g->comm, g->comm_stream), -1);
+    CK(cudaStreamSynchronize(g->comm_stream));
+    std::vector<unsigned char> all(REC * size_t(W));
+    CK(cudaMemcpy(all.data(), g->d_ipc, all.size(), cudaMemcpyDeviceToHost));
+    auto open = [&](int rank, int idx, void **out) -> pr_status {
+        cudaIpcMemHandle_t hh;
+        std::memcpy(&hh, all.data() + REC * size_t(rank) + idx * sizeof hh, sizeof hh);
+        CK(cudaIpcOpenMemHandle(out, hh, cudaIpcMemLazyEnablePeerAccess));
+        g->ipc_open.push_back(*out);
+        return PR_OK;
+    };
+    void *p = nullptr;
+    if (r < W - 1) {
+        CKS(open(r + 1, 0, &p)); g->peer_mail[0] = static_cast<double *>(p);
+        CKS(open(r + 1, 1, &p)); g->peer_mail[1] = static_cast<double *>(p);
+        CKS(open(r + 1, 2, &p)); g->succ_flags = static_cast<unsigned int *>(p);
+    }
+    if (r > 0) {
+        CKS(open(r - 1, 2, &p));
+        g->pred_flags = static_cast<unsigned int *>(p);
+    }
+    g->mapped_gen = g->pool_gen;
+    return PR_OK;
+}
+
+static pr_status stream_wait_geq(cudaStream_t st, const unsigned int *addr, unsigned int v) {
+    CUresult e = stream_wait_fn()(reinterpret_cast<CUstream>(st),
+                                  reinterpret_cast<CUdeviceptr>(addr), v, CU_STREAM_WAIT_VALUE_GEQ);
+    if (e != CUDA_SUCCESS) return fail(PR_ECUDA, "cuStreamWaitValue32 failed (%d)", int(e));
+    return PR_OK;
+}
+
+static pr_status post(pr_grid *g, double *stop_dst, double stop, unsigned int *flag, unsigned int seq,
+                      cudaStream_t st) {
+    post_kernel<<<1, 1, 0, st>>>(stop_dst, stop, flag, seq);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    CKL();
+    return PR_OK;
+}
+
 pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, double *u_T,
                       const double *u_ref, double *defects_host, void *stream) {
     CKS(check_grid(g));
@@ -1108,6 +1203,7 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
             g->pool.push_back(p);
         }
         g->par_s = s;
+        ++g->pool_gen;
     }
     std::vector<double *> start(s), f(s), out(s), gold(s);
     for (int l = 0; l < s; ++l) {
@@ -1117,6 +1213,15 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
         gold[l] = g->pool[3 * s + l];
     }
     double *gnew = g->pool[4 * s], *recvb = g->pool[4 * s + 1], *u0d = g->pool[4 * s + 2];
+    // peer hand-off: the receive buffer alternates between pool[4s+1] (even k) and
+    // pool[0] (odd k: start[0] swaps with recvb at the end of every iteration)
+    const bool peer = (cfg->flags & PR_FLAG_PEER_HANDOFF) && W > 1;
+    unsigned int base = 0;
+    if (peer) {
+        CKS(peer_setup(g, g->pool[4 * s + 1], g->pool[0]));
+        base = g->seq_base;
+        g->seq_base += unsigned(K) + 2;
+    }
     const bool want_def = last && u_ref && defects_host;
     const double *refd = u_ref;
     if (want_def && is_host_ptr(u_ref)) {
@@ -1170,6 +1275,8 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
     };
     const size_t msg = size_t(g->N) + (ctrl ? 1 : 0);  // hand-off length (doubles)
 
+    // peer mode: this rank's receive buffers are idle until its first receive
+    if (peer && r > 0) CKS(post(g, nullptr, 0.0, g->pred_flags + 1, base, st));
     const double *v = u0d;
     bool sent_pending = false, init_marked = false, pred_stopped = (r == 0), stopped = false;
     bool recvd = false;
@@ -1202,6 +1309,9 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
             break;
         case PR_OP_F:
             CKS(Fp(start[l], f[l], op.slice));
+            // peer mode: start[0] (next iteration's receive buffer of the same parity) is free
+            if (peer && r > 0 && l == 0)
+                CKS(post(g, nullptr, 0.0, g->pred_flags + 1, base + unsigned(op.k) + 1, st));
             if (l == s - 1) {
                 CK(cudaEventRecord(evF(op.k), st));
                 CK(cudaEventRecord(fdone_ev, st));
@@ -1210,6 +1320,13 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
         case PR_OP_RECV:
             recvd = false;
             if (pred_stopped) break;  // the predecessor sent its last message earlier
+            if (peer) {  // the predecessor's correction stored straight into recvb
+                CKS(stream_wait_geq(st, g->d_flags + 0, base + unsigned(op.k) + 1));
+                if (ctrl) CK(cudaMemcpyAsync(g->h_flag, recvb + g->N, sizeof(double),
+                                             cudaMemcpyDeviceToHost, st));
+                recvd = true;
+                break;
+            }
             // the receive buffer was last read by F of iteration k-1 (done: stream order)
             CK(cudaStreamWaitEvent(g->comm_stream, fdone_ev, 0));
             NCK(ncclRecv(recvb, msg, ncclDouble, op.peer, g->comm, g->comm_stream), op.k);
@@ -1237,9 +1354,16 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
             // previous iterate of this slice's end value: the coarse guess in
             // iteration 0, else start[l+1] (l < s-1) or out[s-1] itself
             const double *prev = op.k == 0 ? gold[l] : (l < s - 1 ? start[l + 1] : out[s - 1]);
+            // peer mode, hand-off slice: the same pass stores into the successor's
+            // receive buffer once the successor has released it
+            double *pmail = nullptr;
+            if (peer && l == s - 1 && r < W - 1) {
+                CKS(stream_wait_geq(st, g->d_flags + 1, base + unsigned(op.k)));
+                pmail = g->peer_mail[op.k & 1];
+            }
             CKS(launch_correct(g, f[l], gnew, gold[l], out[l], fuse ? refd : nullptr,
                                g->d_red + op.k + 1, st, prev, red_chg + 2 * op.k,
-                               red_chg + 2 * op.k + 1));
+                               red_chg + 2 * op.k + 1, pmail));
             std::swap(gold[l], gnew);
             if (l == s - 1) {  // end of this rank's iteration: the stop decision
                 iters = op.k + 1;
@@ -1253,17 +1377,21 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
                     g->monitors[op.k] = ch;
                     if (recvd && g->h_flag[0] != 0.0) pred_stopped = true;
                     if (pred_stopped && ch <= tol) stop_now = true;
-                    if (r < W - 1) {  // the flag rides on this iteration's message
+                    if (r < W - 1 && !peer) {  // the flag rides on this iteration's message
                         set_flag_kernel<<<1, 1, 0, st>>>(out[s - 1] + g->N, stop_now ? 1.0 : 0.0);
                         g_launches.fetch_add(1, std::memory_order_relaxed);
                         CKL();
                     }
                 }
+                if (peer && r < W - 1)  // publish: stop flag, then the data sequence word
+                    CKS(post(g, ctrl ? pmail + g->N : nullptr, stop_now ? 1.0 : 0.0,
+                             g->succ_flags + 0, base + unsigned(op.k) + 1, st));
                 if (stop_now) stopped = true;
             }
             break;
         }
         case PR_OP_SEND:
+            if (peer) break;  // stored by the correction kernel, published by post_kernel
             CK(cudaEventRecord(corr_ev(op.k), st));
             CK(cudaStreamWaitEvent(g->comm_stream, corr_ev(op.k), 0));
             NCK(ncclSend(out[s - 1], msg, ncclDouble, op.peer, g->comm, g->comm_stream), op.k);
@@ -1282,7 +1410,7 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
         }
         // a rank that stops still sends its last message (and records its iteration end)
         if (stopped && op.op == PR_OP_CORRECT && op.slice == j0 + s - 1) {
-            if (r < W - 1) {
+            if (r < W - 1 && !peer) {
                 CK(cudaEventRecord(corr_ev(op.k), st));
                 CK(cudaStreamWaitEvent(g->comm_stream, corr_ev(op.k), 0));
                 NCK(ncclSend(out[s - 1], msg, ncclDouble, r + 1, g->comm, g->comm_stream), op.k);

@@ -1,4 +1,4 @@
-"""Multi-GPU Parareal (NCCL hand-off) — runs tools/mgpu_check.py under torchrun
+"""Multi-GPU Parareal (NCCL or peer-store hand-off) — runs tools/mgpu_check.py under torchrun
 when at least 2 GPUs are visible; W-invariance is bitwise, oracle parity 1e-12."""
 import json
 import os
@@ -25,15 +25,23 @@ def ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("W,n,Np,K,tol", [(2, 32, 4, 2, 0.0), (2, 32, 2, 2, 0.0), (2, 40, 4, 3, 0.0),
-                                          (4, 32, 4, 2, 0.0), (4, 32, 8, 3, 0.0), (8, 32, 8, 3, 0.0),
-                                          (2, 128, 2, 1, 0.0), (2, 32, 4, 4, 3e-3), (4, 32, 4, 4, 3e-3)])
-def test_parareal_multi_gpu(W, n, Np, K, tol):
+CASES = [(2, 32, 4, 2, 0.0), (2, 32, 2, 2, 0.0), (2, 40, 4, 3, 0.0), (4, 32, 4, 2, 0.0), (4, 32, 8, 3, 0.0),
+         (8, 32, 8, 3, 0.0), (2, 128, 2, 1, 0.0), (2, 32, 4, 4, 3e-3), (4, 32, 4, 4, 3e-3)]
+PEER = [(2, 32, 4, 2, 0.0), (2, 40, 4, 3, 0.0), (4, 32, 8, 3, 0.0), (2, 128, 2, 1, 0.0),
+        (2, 32, 4, 4, 3e-3), (4, 32, 4, 4, 3e-3)]
+
+
+@pytest.mark.parametrize("W,n,Np,K,tol,handoff", [c + ("nccl",) for c in CASES] + [c + ("peer",) for c in PEER])
+def test_parareal_multi_gpu(W, n, Np, K, tol, handoff):
+    """Each case runs pr_parareal twice (second call: same buffers, next sequence
+    epoch) and compares with one GPU (bitwise) and the oracle.  `peer`: the
+    correction kernel stores the hand-off into the successor's buffer over
+    NVLink (PR_FLAG_PEER_HANDOFF) instead of ncclSend/ncclRecv."""
     if ngpus() < W:
         pytest.skip(f"needs {W} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={W}",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
-           os.path.join(ROOT, "tools", "mgpu_check.py"), str(n), str(Np), str(K), str(tol)]
+           os.path.join(ROOT, "tools", "mgpu_check.py"), str(n), str(Np), str(K), str(tol), handoff]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
     assert res.returncode == 0 and lines, res.stdout[-3000:] + res.stderr[-3000:]
