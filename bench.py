@@ -227,6 +227,9 @@ def main():
     ap.add_argument("--handoff", default="peer", choices=["nccl", "peer"],
                     help="hand-off of u^{k+1} between ranks: ncclSend/Recv or peer stores "
                          "from the correction kernel (PR_FLAG_PEER_HANDOFF)")
+    ap.add_argument("--g-mesh", default="full", choices=["full", "half"],
+                    help="G on the fine mesh (Alg.2, the paper's) or on the n/2 mesh with "
+                         "restriction / prolongation (NEXT-4, PR_FLAG_G_HALF_MESH)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--nu-mode", type=int, default=None)
@@ -307,9 +310,17 @@ def main():
         Q_s = (j1 - j0) if (j0 is not None and j1 is not None) else None
         C_f_ms = e0.elapsed_time(e1)
         tau_f = C_f_ms / cfg.Nt
-        e0.record(stream)
-        pr.pr_coarse(grid, u0, uT, 0, cfg.NC, Dt)
-        e1.record(stream)
+        if args.g_mesh == "half":  # per-slice G_c calls (restriction + prolongation each)
+            pr.pr_coarse_mesh(grid, u0, uT, 0, 8, Dt)
+            torch.cuda.synchronize(dev)
+            e0.record(stream)
+            for m in range(Np):
+                pr.pr_coarse_mesh(grid, u0, uT, m * nc, nc, Dt)
+            e1.record(stream)
+        else:
+            e0.record(stream)
+            pr.pr_coarse(grid, u0, uT, 0, cfg.NC, Dt)
+            e1.record(stream)
         torch.cuda.synchronize(dev)
         tau_c = e0.elapsed_time(e1) / cfg.NC
     tf_all = max_over_ranks(tau_f)
@@ -317,7 +328,8 @@ def main():
     C_f_ms = max_over_ranks(C_f_ms)
 
     pcfg = pr.PararealCfg(Np, nc, nf, K, tol=args.tol,
-                          flags=pr.PR_FLAG_PEER_HANDOFF if args.handoff == "peer" else 0)
+                          flags=(pr.PR_FLAG_PEER_HANDOFF if args.handoff == "peer" else 0)
+                          | (pr.PR_FLAG_G_HALF_MESH if args.g_mesh == "half" else 0))
     for _ in range(args.warmup):
         pr.pr_parareal(grid, pcfg, u0, uT if last else None, uref)
     barrier()
@@ -431,6 +443,7 @@ def main():
                        "c": list(cfg.c), "parallelism": f"time-parallel Parareal, {world} GPU(s), "
                                                         f"{Np // world} slice(s)/GPU",
                        "handoff": args.handoff if world > 1 else "none",
+                       "g_mesh": args.g_mesh,
                        "l2": "inputs larger than L2 (128 MiB fields at 256^3)" if n >= 256 else
                              "fields L2-resident"},
             "speedup": {"S_measured": S_meas, "S_bound_eq_speedup_P229": S_bound,

@@ -81,12 +81,14 @@ typedef struct {
     int32_t n_fine_per_slice;    /* N_f >= 1, delta t = T / (N_p N_f) */
     int32_t K;                   /* iterations k_max >= 0 (K = 0: coarse guess only) */
     int32_t flags;               /* bit 0 (PR_FLAG_G_IS_F): use F for G (degenerate test);
-                                    bit 1 (PR_FLAG_PEER_HANDOFF): hand-off by peer stores (below) */
+                                    bit 1 (PR_FLAG_PEER_HANDOFF): hand-off by peer stores (below);
+                                    bit 2 (PR_FLAG_G_HALF_MESH): G = pr_coarse_mesh's G_c */
     double tol;                  /* > 0: convergence-controlled stopping (below); <= 0: fixed K */
 } pr_parareal_cfg;
 
 #define PR_FLAG_G_IS_F 1
 #define PR_FLAG_PEER_HANDOFF 2
+#define PR_FLAG_G_HALF_MESH 4
 
 typedef struct pr_grid pr_grid;  /* opaque */
 
@@ -124,6 +126,17 @@ pr_status pr_defect(pr_grid *grid, const double *u, const double *u_ref, double 
 
 /* u = sin(2 pi x) sin(2 pi y) sin(2 pi z), device pointer. */
 pr_status pr_fill_sine(pr_grid *grid, double *u, void *stream);
+
+/* Spatially coarsened coarse propagator G_c (P:238-241 names
+ * coarsening in space as a cheaper G without fixing the transfer operators;
+ * readings DESIGN.md C24-C26): restriction by injection onto the n/2 mesh
+ * (uc[k][j][i] = u[2k][2j][2i]), n_steps Alg.2 Euler steps there (dx = 2/n,
+ * the same Delta t and nu_j = nu(j dt)), periodic trilinear prolongation back
+ * to n^3 (each fine point the mean of its 1, 2, 4 or 8 coarse neighbours).
+ * Same argument conventions as pr_coarse; needs n % 4 == 0 (PR_EINVAL).  The
+ * n/2 mesh lives in a child grid allocated at the first call. */
+pr_status pr_coarse_mesh(pr_grid *grid, const double *u_in, double *u_out, int64_t step0,
+                         int64_t n_steps, double dt, void *stream);
 
 /* Parareal correction (Alg.1 line alg_para_corr):
  *   u_out = f + (g_new - g_old)          (rounding order: DESIGN.md C5)

@@ -87,7 +87,10 @@ def lib():
             "orc_parareal": (ctypes.c_int, [P, i32, i32, i32, i32, _D, _D, _D, _D, i32]),
             "orc_threads": (ctypes.c_int, []),
             "orc_parareal_tol": (ctypes.c_int, [P, i32, i32, i32, i32, dbl, i32, _D, _D, _D, _D, _D,
-                                                ctypes.POINTER(ctypes.c_int32)]),
+                                                ctypes.POINTER(ctypes.c_int32), i32]),
+            "orc_restrict": (None, [i32, _D, _D]),
+            "orc_prolong": (None, [i32, _D, _D]),
+            "orc_coarse_mesh": (None, [P, _D, i64, i64, dbl]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -155,6 +158,32 @@ def coarse(p: Problem, u: np.ndarray, step0: int, n_steps: int, dt: float) -> np
     return v
 
 
+def restrict(u: np.ndarray) -> np.ndarray:
+    """Injection onto the n/2 mesh (C24)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    n = u.shape[0]
+    uc = _field(n // 2)
+    lib().orc_restrict(n, _ptr(u), _ptr(uc))
+    return uc
+
+
+def prolong(uc: np.ndarray) -> np.ndarray:
+    """Periodic trilinear prolongation from the n/2 mesh (C25)."""
+    uc = np.ascontiguousarray(uc, dtype=np.float64)
+    n = 2 * uc.shape[0]
+    u = _field(n)
+    lib().orc_prolong(n, _ptr(uc), _ptr(u))
+    return u
+
+
+def coarse_mesh(p: Problem, u: np.ndarray, step0: int, n_steps: int, dt: float) -> np.ndarray:
+    """G_c = prolong o (Alg.2 on the n/2 mesh) o restrict (C26)."""
+    v = np.array(u, dtype=np.float64, order="C", copy=True)
+    pc = p._c()
+    lib().orc_coarse_mesh(ctypes.byref(pc), _ptr(v), step0, n_steps, dt)
+    return v
+
+
 def fine(p: Problem, u: np.ndarray, step0: int, n_steps: int, dt: float) -> np.ndarray:
     """F over global steps [step0, step0+n_steps) (classical RK4)."""
     v = np.array(u, dtype=np.float64, order="C", copy=True)
@@ -182,7 +211,7 @@ class PararealResult:
 
 def parareal(p: Problem, n_slices: int, nc: int, nf: int, K: int,
              u0: np.ndarray | None = None, u_ref: np.ndarray | None = None,
-             g_is_f: bool = False) -> PararealResult:
+             g_is_f: bool = False, g_half_mesh: bool = False) -> PararealResult:
     """Alg.1 for all ranks, executed serially in pipeline order."""
     u0 = initial(p.n) if u0 is None else np.ascontiguousarray(u0, dtype=np.float64)
     uT = _field(p.n)
@@ -190,7 +219,7 @@ def parareal(p: Problem, n_slices: int, nc: int, nf: int, K: int,
     pc = p._c()
     rc = lib().orc_parareal(ctypes.byref(pc), n_slices, nc, nf, K, _ptr(u0),
                             _ptr(np.ascontiguousarray(u_ref)) if u_ref is not None else None,
-                            _ptr(uT), _ptr(d), 1 if g_is_f else 0)
+                            _ptr(uT), _ptr(d), (1 if g_is_f else 0) | (4 if g_half_mesh else 0))
     if rc != 0:
         raise ValueError("orc_parareal: bad arguments")
     return PararealResult(uT, d if u_ref is not None else None)
@@ -205,7 +234,8 @@ class PararealTolResult:
 
 
 def parareal_tol(p: Problem, n_slices: int, nc: int, nf: int, K: int, tol: float, world: int,
-                 u0: np.ndarray | None = None, u_ref: np.ndarray | None = None) -> PararealTolResult:
+                 u0: np.ndarray | None = None, u_ref: np.ndarray | None = None,
+                 g_half_mesh: bool = False) -> PararealTolResult:
     """Alg.1 with the convergence-controlled stop rule of DESIGN.md C23."""
     u0 = initial(p.n) if u0 is None else np.ascontiguousarray(u0, dtype=np.float64)
     uT = _field(p.n)
@@ -215,7 +245,7 @@ def parareal_tol(p: Problem, n_slices: int, nc: int, nf: int, K: int, tol: float
     pc = p._c()
     rc = lib().orc_parareal_tol(ctypes.byref(pc), n_slices, nc, nf, K, tol, world, _ptr(u0),
                                 _ptr(np.ascontiguousarray(u_ref)) if u_ref is not None else None,
-                                _ptr(uT), _ptr(d), _ptr(ch), it)
+                                _ptr(uT), _ptr(d), _ptr(ch), it, 4 if g_half_mesh else 0)
     if rc != 0:
         raise ValueError("orc_parareal_tol: bad arguments")
     return PararealTolResult(uT, d, ch.reshape(world, K), np.array(list(it)))

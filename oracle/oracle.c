@@ -180,6 +180,54 @@ void orc_coarse(const orc_problem *p, double *u, int64_t step0, int64_t n_steps,
     free(rhs);
 }
 
+/* Restriction by injection (C24): the n/2 mesh points x_i = i/(n/2) are the
+ * even fine points. */
+void orc_restrict(int32_t n_, const double *u, double *uc) {
+    const int64_t n = n_, m = n / 2;
+    for (int64_t k = 0; k < m; ++k)
+        for (int64_t j = 0; j < m; ++j)
+            for (int64_t i = 0; i < m; ++i)
+                uc[(k * m + j) * m + i] = u[((2 * k) * n + 2 * j) * n + 2 * i];
+}
+
+/* Trilinear prolongation (C25), written as the average over the coarse
+ * neighbours of every fine point: along an axis with even fine index the one
+ * coarse point i/2, along an odd one the two points (i-1)/2 and (i+1)/2
+ * (periodic).  The sum runs over the 1, 2, 4 or 8 combinations in the order
+ * z-, y-, x-candidate (outer to inner) and is divided by their count. */
+void orc_prolong(int32_t n_, const double *uc, double *u) {
+    const int64_t n = n_, m = n / 2;
+    for (int64_t k = 0; k < n; ++k)
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t i = 0; i < n; ++i) {
+                int64_t ks[2], js[2], is[2];
+                const int nk = (k % 2) ? 2 : 1, nj = (j % 2) ? 2 : 1, ni = (i % 2) ? 2 : 1;
+                ks[0] = k / 2; ks[1] = (k / 2 + 1) % m;
+                js[0] = j / 2; js[1] = (j / 2 + 1) % m;
+                is[0] = i / 2; is[1] = (i / 2 + 1) % m;
+                double sum = 0.0;
+                for (int a = 0; a < nk; ++a)
+                    for (int b = 0; b < nj; ++b)
+                        for (int c = 0; c < ni; ++c)
+                            sum += uc[(ks[a] * m + js[b]) * m + is[c]];
+                u[(k * n + j) * n + i] = sum / (double)(nk * nj * ni);
+            }
+}
+
+/* G_c (C26): restrict, Alg.2 on the n/2 mesh (dx = 2/n, same dt and nu_j),
+ * prolongate; u (fine mesh) is overwritten. */
+void orc_coarse_mesh(const orc_problem *p, double *u, int64_t step0, int64_t n_steps,
+                     double dt) {
+    const int64_t m = p->n / 2;
+    double *uc = (double *)malloc(sizeof(double) * (size_t)(m * m * m));
+    orc_problem pc = *p;
+    pc.n = (int32_t)m;
+    orc_restrict(p->n, u, uc);
+    orc_coarse(&pc, uc, step0, n_steps, dt);
+    orc_prolong(p->n, uc, u);
+    free(uc);
+}
+
 /* Classical RK4:
  *   k1 = f(u, t1), k2 = f(u + dt/2 k1, t2), k3 = f(u + dt/2 k2, t3),
  *   k4 = f(u + dt k3, t4),  u <- u + dt/6 (k1 + 2 k2 + 2 k3 + k4). */
@@ -242,6 +290,8 @@ static void G_slice(const orc_problem *p, int32_t flags, double *u, int64_t m,
                     int64_t nc, int64_t nf, double Dt, double dt) {
     if (flags & 1)
         orc_fine(p, u, m * nf, nf, dt); /* degenerate test: G := F */
+    else if (flags & 4)
+        orc_coarse_mesh(p, u, m * nc, nc, Dt); /* G_c on the n/2 mesh (NEXT-4) */
     else
         orc_coarse(p, u, m * nc, nc, Dt);
 }
@@ -255,7 +305,8 @@ static void F_slice(const orc_problem *p, double *u, int64_t m, int64_t nf,
 int orc_parareal(const orc_problem *p, int32_t n_slices, int32_t nc_, int32_t nf_,
                  int32_t K, const double *u0, const double *u_ref, double *u_T,
                  double *defects, int32_t flags) {
-    if (!p || !u0 || !u_T || n_slices < 1 || nc_ < 1 || nf_ < 1 || K < 0 || p->n < 1)
+    if (!p || !u0 || !u_T || n_slices < 1 || nc_ < 1 || nf_ < 1 || K < 0 || p->n < 1 ||
+        ((flags & 4) && p->n % 4))
         return -1;
     const int64_t n = p->n, N = n * n * n, Np = n_slices, nc = nc_, nf = nf_;
     const double Dt = p->T / (double)(Np * nc); /* coarse step  Delta t */
@@ -325,9 +376,10 @@ int orc_parareal(const orc_problem *p, int32_t n_slices, int32_t nc_, int32_t nf
  * executed in pipeline order: iteration-major, rank-minor. */
 int orc_parareal_tol(const orc_problem *p, int32_t n_slices, int32_t nc_, int32_t nf_, int32_t K,
                      double tol, int32_t world, const double *u0, const double *u_ref,
-                     double *u_T, double *defects, double *changes, int32_t *iters) {
+                     double *u_T, double *defects, double *changes, int32_t *iters,
+                     int32_t flags) {
     if (!p || !u0 || !u_T || n_slices < 1 || nc_ < 1 || nf_ < 1 || K < 0 || world < 1 ||
-        n_slices % world || p->n < 1 || !(tol >= 0.0))
+        n_slices % world || p->n < 1 || !(tol >= 0.0) || ((flags & 4) && p->n % 4))
         return -1;
     const int64_t n = p->n, N = n * n * n, Np = n_slices, nc = nc_, nf = nf_, W = world,
                   s = n_slices / world;
@@ -352,7 +404,7 @@ int orc_parareal_tol(const orc_problem *p, int32_t n_slices, int32_t nc_, int32_
         memcpy(u_p[0], u0, bytes);
         for (int64_t j = 0; j < Np; ++j) {
             memcpy(ut_old[j], u_p[j], bytes);
-            G_slice(p, 0, ut_old[j], j, nc, nf, Dt, dt);
+            G_slice(p, flags, ut_old[j], j, nc, nf, Dt, dt);
             memcpy(out[j], ut_old[j], bytes);
             if (j + 1 < Np) memcpy(u_p[j + 1], ut_old[j], bytes);
         }
@@ -378,7 +430,7 @@ int orc_parareal_tol(const orc_problem *p, int32_t n_slices, int32_t nc_, int32_
                     if (j == 0) memcpy(u_in, u0, bytes);
                     else memcpy(u_in, out[j - 1], bytes);
                     memcpy(ut_new, u_in, bytes);
-                    G_slice(p, 0, ut_new, j, nc, nf, Dt, dt);
+                    G_slice(p, flags, ut_new, j, nc, nf, Dt, dt);
                     for (int64_t q = 0; q < N; ++q) neu[q] = uhat[q] + (ut_new[q] - ut_old[j][q]);
                     const double dm = orc_inf_diff(p->n, neu, out[j]), um = orc_inf_norm(p->n, neu);
                     if (dm > dmax || dm != dm) dmax = dm;

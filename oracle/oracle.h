@@ -62,6 +62,21 @@ void orc_coarse(const orc_problem *p, double *u, int64_t step0, int64_t n_steps,
 void orc_fine(const orc_problem *p, double *u, int64_t step0, int64_t n_steps,
               double dt);
 
+/* Spatially coarsened G (P:238-241 names coarsening in space
+ * as a way to make G cheaper, without fixing the transfer operators; readings
+ * DESIGN.md C24-C26).  n must be a multiple of 4 (the n/2 mesh is even).
+ *   restriction  (C24, injection):  uc[k][j][i] = u[2k][2j][2i]
+ *   prolongation (C25, trilinear, periodic): the value at fine point
+ *     (i, j, k) is the average over the coarse points (floor(i/2) or
+ *     floor(i/2) + 1 along every axis with odd index; the index itself along
+ *     every axis with even index), i.e. 1, 2, 4 or 8 coarse values with equal
+ *     weights 1/2, 1/4, 1/8
+ *   G_c = P o (Alg.2 on the n/2 mesh, same Delta t and nu_j) o R   (C26)  */
+void orc_restrict(int32_t n, const double *u, double *uc);
+void orc_prolong(int32_t n, const double *uc, double *u);
+void orc_coarse_mesh(const orc_problem *p, double *u, int64_t step0, int64_t n_steps,
+                     double dt);
+
 /* max |u| over the n^3 points (the ||.||_inf of Eq.(defect)). */
 double orc_inf_norm(int32_t n, const double *u);
 /* max |u - v| */
@@ -74,7 +89,8 @@ double orc_defect(int32_t n, const double *u, const double *ref);
  * T/(n_slices*nf) and coarse steps [m*nc, (m+1)*nc) of size T/(n_slices*nc).
  * u_T receives u^K_{N_p}.  defects (K+1 entries, may be NULL) receives
  * d^0..d^K against u_ref (may be NULL; then defects is left untouched).
- * flags bit 0: use F in place of G (degenerate test case).
+ * flags bit 0: use F in place of G (degenerate test case);
+ * bit 2: use the spatially coarsened G_c (orc_coarse_mesh) as G.
  * Returns 0, or -1 on bad arguments / allocation failure. */
 int orc_parareal(const orc_problem *p, int32_t n_slices, int32_t nc, int32_t nf,
                  int32_t K, const double *u0, const double *u_ref, double *u_T,
@@ -96,7 +112,8 @@ int orc_parareal(const orc_problem *p, int32_t n_slices, int32_t nc, int32_t nf,
  * the fixed-K algorithm. */
 int orc_parareal_tol(const orc_problem *p, int32_t n_slices, int32_t nc, int32_t nf, int32_t K,
                      double tol, int32_t world, const double *u0, const double *u_ref,
-                     double *u_T, double *defects, double *changes, int32_t *iters);
+                     double *u_T, double *defects, double *changes, int32_t *iters,
+                     int32_t flags);
 
 /* Threads the OpenMP runtime will use (1 when built without OpenMP). */
 int orc_threads(void);

@@ -15,14 +15,16 @@ import ctypes
 from dataclasses import dataclass
 
 from . import _lib
-from ._lib import (PR_NU_STAGE, PR_NU_STEP_START, PR_FLAG_G_IS_F, PR_FLAG_PEER_HANDOFF, PrError, OPS,
+from ._lib import (PR_NU_STAGE, PR_NU_STEP_START, PR_FLAG_G_IS_F, PR_FLAG_PEER_HANDOFF,
+                   PR_FLAG_G_HALF_MESH, PrError, OPS,
                    PR_NCCL_ID_BYTES)
 
 __all__ = ["Problem", "PararealCfg", "Grid", "pr_create_grid", "pr_destroy_grid", "pr_fine",
            "pr_coarse", "pr_defect", "pr_fill_sine", "pr_correct", "pr_nccl_unique_id",
            "pr_comm_init", "pr_parareal", "pr_plan", "pr_last_timings", "pr_kernel_launches",
            "pr_stability_ratio", "pr_last_error", "pr_version", "pr_grid_info", "pr_last_monitors", "PrError", "PR_NU_STAGE",
-           "PR_NU_STEP_START", "PR_FLAG_G_IS_F", "PR_FLAG_PEER_HANDOFF", "comm_init_torch"]
+           "PR_NU_STEP_START", "PR_FLAG_G_IS_F", "PR_FLAG_PEER_HANDOFF", "PR_FLAG_G_HALF_MESH",
+           "pr_coarse_mesh", "comm_init_torch"]
 
 
 @dataclass
@@ -138,6 +140,9 @@ class Grid:
     def pr_coarse(self, u_in, u_out, step0, n_steps, dt, stream=None):
         return pr_coarse(self, u_in, u_out, step0, n_steps, dt, stream)
 
+    def pr_coarse_mesh(self, u_in, u_out, step0, n_steps, dt, stream=None):
+        return pr_coarse_mesh(self, u_in, u_out, step0, n_steps, dt, stream)
+
     def pr_defect(self, u, u_ref, stream=None):
         return pr_defect(self, u, u_ref, stream)
 
@@ -177,6 +182,13 @@ def pr_coarse(grid, u_in, u_out, step0: int, n_steps: int, dt: float, stream=Non
     _size_check(grid, u_in, u_out)
     _lib.check(_lib.load().pr_coarse(grid.handle, _ptr(u_in), _ptr(u_out), int(step0), int(n_steps),
                                      float(dt), _stream(stream, u_in, u_out)))
+
+
+def pr_coarse_mesh(grid, u_in, u_out, step0: int, n_steps: int, dt: float, stream=None) -> None:
+    """G_c: restriction, Alg.2 on the n/2 mesh, trilinear prolongation (NEXT-4)."""
+    _size_check(grid, u_in, u_out)
+    _lib.check(_lib.load().pr_coarse_mesh(grid.handle, _ptr(u_in), _ptr(u_out), int(step0),
+                                          int(n_steps), float(dt), _stream(stream, u_in, u_out)))
 
 
 def pr_defect(grid, u, u_ref, stream=None) -> float:

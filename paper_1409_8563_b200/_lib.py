@@ -18,12 +18,13 @@ STATUS_NAMES = {0: "PR_OK", 1: "PR_EINVAL", 2: "PR_ENOMEM", 3: "PR_ECUDA", 4: "P
 PR_NU_STAGE, PR_NU_STEP_START = 0, 1
 PR_FLAG_G_IS_F = 1
 PR_FLAG_PEER_HANDOFF = 2
+PR_FLAG_G_HALF_MESH = 4
 PR_NCCL_ID_BYTES = 128
 OPS = {1: "G_PREFIX", 2: "G_INIT", 3: "DEFECT0", 4: "F", 5: "RECV", 6: "G", 7: "CORRECT",
        8: "SEND", 9: "END_ITER"}
 
 # Every symbol include/parareal.h declares (checked by tests/test_abi.py).
-EXPORTS = ["pr_create_grid", "pr_destroy_grid", "pr_fine", "pr_coarse", "pr_defect",
+EXPORTS = ["pr_create_grid", "pr_destroy_grid", "pr_fine", "pr_coarse", "pr_coarse_mesh", "pr_defect",
            "pr_fill_sine", "pr_correct", "pr_nccl_unique_id", "pr_comm_init", "pr_parareal",
            "pr_plan", "pr_last_timings", "pr_kernel_launches", "pr_stability_ratio",
            "pr_last_error", "pr_version", "pr_grid_info", "pr_last_monitors"]
@@ -75,6 +76,7 @@ def load() -> ctypes.CDLL:
         "pr_destroy_grid": (st, [vp]),
         "pr_fine": (st, [vp, vp, vp, i64, i64, dbl, vp]),
         "pr_coarse": (st, [vp, vp, vp, i64, i64, dbl, vp]),
+        "pr_coarse_mesh": (st, [vp, vp, vp, i64, i64, dbl, vp]),
         "pr_defect": (st, [vp, vp, vp, ctypes.POINTER(dbl), vp]),
         "pr_fill_sine": (st, [vp, vp, vp]),
         "pr_correct": (st, [vp, vp, vp, vp, vp, vp, ctypes.POINTER(dbl), vp]),

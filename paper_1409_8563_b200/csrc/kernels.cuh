@@ -419,6 +419,40 @@ correct_kernel(const double2 *__restrict__ f, const double2 *__restrict__ gn,
 // set the stop-flag element that trails a hand-off buffer (C23)
 __global__ void set_flag_kernel(double *p, double v) { *p = v; }
 
+// Spatially coarsened G (NEXT-4, C24-C26).  Restriction by injection
+// onto the n/2 mesh: uc[k][j][i] = u[2k][2j][2i] (one thread per coarse point).
+__global__ void restrict_kernel(const double *__restrict__ u, double *__restrict__ uc, int n) {
+    const int m = n / 2;
+    const long long total = (long long)m * m * m;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+         q += (long long)gridDim.x * blockDim.x) {
+        const int i = int(q % m), j = int((q / m) % m), k = int(q / ((long long)m * m));
+        uc[q] = u[((2LL * k) * n + 2 * j) * n + 2 * i];
+    }
+}
+// Periodic trilinear prolongation: every fine point is the mean of its 1, 2, 4
+// or 8 coarse neighbours (index/2 along even axes; index/2 and index/2+1 along
+// odd ones), summed z-, y-, x-candidate outer to inner, then divided by the count.
+__global__ void prolong_kernel(const double *__restrict__ uc, double *__restrict__ u, int n) {
+    const int m = n / 2;
+    const long long total = (long long)n * n * n;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+         q += (long long)gridDim.x * blockDim.x) {
+        const int i = int(q % n), j = int((q / n) % n), k = int(q / ((long long)n * n));
+        const int nk = (k & 1) + 1, nj = (j & 1) + 1, ni = (i & 1) + 1;
+        const int k0 = k >> 1, j0 = j >> 1, i0 = i >> 1;
+        const int ks[2] = {k0, k0 + 1 == m ? 0 : k0 + 1};
+        const int js[2] = {j0, j0 + 1 == m ? 0 : j0 + 1};
+        const int is[2] = {i0, i0 + 1 == m ? 0 : i0 + 1};
+        double sum = 0.0;
+        for (int a = 0; a < nk; ++a)
+            for (int b = 0; b < nj; ++b)
+                for (int c = 0; c < ni; ++c)
+                    sum += uc[((long long)ks[a] * m + js[b]) * m + is[c]];
+        u[q] = sum / double(nk * nj * ni);
+    }
+}
+
 // Peer hand-off publication (one thread): optional stop flag into the peer's
 // message tail, then the sequence word with system-scope release semantics, so
 // every store of the preceding kernels in this stream (the correction's peer

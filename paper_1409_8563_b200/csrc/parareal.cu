@@ -132,6 +132,9 @@ struct pr_grid {
     std::vector<void *> ipc_open;
     long long pool_gen = 0, mapped_gen = -1;
     unsigned int seq_base = 0;              // advances by K + 2 per peer-mode pr_parareal
+    // spatially coarsened G (NEXT-4): a child grid on the n/2 mesh and one field there
+    pr_grid *half = nullptr;
+    double *half_u = nullptr;
 };
 
 // cuStreamWaitValue32 through the runtime's driver entry point: the stream's
@@ -820,6 +823,9 @@ pr_status pr_destroy_grid(pr_grid *g) {
     g->graphs.clear();
     for (void *p : g->ipc_open) cudaIpcCloseMemHandle(p);
     cudaFree(g->d_flags); cudaFree(g->d_ipc);
+    if (g->half) pr_destroy_grid(g->half);
+    cudaFree(g->half_u);
+    cudaSetDevice(g->dev);
     if (g->comm) ncclCommDestroy(g->comm);
     for (double *p : g->pool) cudaFree(p);
     cudaFree(g->acc); cudaFree(g->ya); cudaFree(g->yb); cudaFree(g->ctmp);
@@ -835,6 +841,29 @@ pr_status pr_destroy_grid(pr_grid *g) {
     if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
     if (g->comm_stream) cudaStreamDestroy(g->comm_stream);
     delete g;
+    return PR_OK;
+}
+
+// G_c = prolong o (Alg.2 on the n/2 mesh) o restrict  (NEXT-4, C24-C26).
+// The n/2 mesh is a child grid with its own nu table, tiles and graphs.
+static pr_status run_coarse_mesh(pr_grid *g, const double *uin, double *uout, int64_t step0,
+                                 int64_t nsteps, double dt, cudaStream_t st) {
+    if (g->n % 4) return fail(PR_EINVAL, "coarse-mesh G needs n %% 4 == 0 (n = %d)", g->n);
+    if (!g->half) {
+        pr_problem hp = g->prob;
+        hp.n = g->n / 2;
+        CKS(pr_create_grid(&hp, g->dev, &g->half));
+        const size_t m = size_t(g->n / 2);
+        CK(cudaMalloc(&g->half_u, m * m * m * sizeof(double)));
+    }
+    const int blocks = g->sms * 8;
+    restrict_kernel<<<blocks, 256, 0, st>>>(uin, g->half_u, g->n);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    CKL();
+    CKS(run_coarse(g->half, g->half_u, g->half_u, step0, nsteps, dt, st));
+    prolong_kernel<<<blocks, 256, 0, st>>>(g->half_u, uout, g->n);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    CKL();
     return PR_OK;
 }
 
@@ -858,8 +887,9 @@ static pr_status propagate(pr_grid *g, int fine, const double *u_in, double *u_o
         }
         if (hout) dout = (hin && u_in == u_out) ? g->stage_a : g->stage_b;
     }
-    CKS(fine ? run_fine(g, din, dout, step0, nsteps, dt, st)
-             : run_coarse(g, din, dout, step0, nsteps, dt, st));
+    CKS(fine == 1   ? run_fine(g, din, dout, step0, nsteps, dt, st)
+        : fine == 2 ? run_coarse_mesh(g, din, dout, step0, nsteps, dt, st)
+                    : run_coarse(g, din, dout, step0, nsteps, dt, st));
     if (hout) {
         CK(cudaMemcpyAsync(u_out, dout, g->bytes, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -877,6 +907,11 @@ pr_status pr_fine(pr_grid *g, const double *u_in, double *u_out, int64_t step0, 
 pr_status pr_coarse(pr_grid *g, const double *u_in, double *u_out, int64_t step0,
                     int64_t n_steps, double dt, void *stream) {
     return propagate(g, 0, u_in, u_out, step0, n_steps, dt, stream);
+}
+
+pr_status pr_coarse_mesh(pr_grid *g, const double *u_in, double *u_out, int64_t step0,
+                         int64_t n_steps, double dt, void *stream) {
+    return propagate(g, 2, u_in, u_out, step0, n_steps, dt, stream);
 }
 
 static pr_status launch_maxabs(pr_grid *g, const double *u, const double *ref,
@@ -1169,6 +1204,8 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
     const int Np = cfg->n_slices, nc = cfg->n_coarse_per_slice, nf = cfg->n_fine_per_slice,
               K = cfg->K;
     const bool g_is_f = (cfg->flags & PR_FLAG_G_IS_F) != 0;
+    const bool g_half = !g_is_f && (cfg->flags & PR_FLAG_G_HALF_MESH) != 0;
+    if (g_half && g->n % 4) return fail(PR_EINVAL, "PR_FLAG_G_HALF_MESH needs n %% 4 == 0");
     const double tol = cfg->tol;
     const bool ctrl = tol > 0.0;  // convergence-controlled stopping (C23)
     if (Np < 1 || nc < 1 || nf < 1 || K < 0 || !(tol == tol))
@@ -1268,6 +1305,7 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
 
     auto G = [&](const double *in, double *o, int m) -> pr_status {
         if (g_is_f) return run_fine(g, in, o, int64_t(m) * nf, nf, dt, st);
+        if (g_half) return run_coarse_mesh(g, in, o, int64_t(m) * nc, nc, Dt, st);
         return run_coarse(g, in, o, int64_t(m) * nc, nc, Dt, st);
     };
     auto Fp = [&](const double *in, double *o, int m) -> pr_status {

@@ -319,3 +319,40 @@ def test_parareal_convergence_control(pick):
     pr.pr_parareal(g, pr.PararealCfg(Np, nc, nf, K), dev(u0), uT, dev(uf))
     mon, iters = pr.pr_last_monitors(g)
     assert iters == K and np.max(np.abs(np.array(mon) - ch)) <= 1e-10
+
+
+# ------------------------------------------- spatially coarsened G (NEXT-4)
+@pytest.mark.parametrize("n", [8, 32, 40, 64, 128])
+def test_coarse_mesh_steps(n):
+    """pr_coarse_mesh (restriction, Alg.2 on the n/2 mesh, prolongation) vs the
+    oracle's G_c, out of place and in place, odd and even step counts."""
+    u0 = random_field(n, 50)
+    g = grid(n)
+    Dt = 5e-4 * (32 / n) ** 2
+    for step0, steps in ((0, 1), (3, 2), (9, 37)):
+        out = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+        pr.pr_coarse_mesh(g, dev(u0), out, step0, steps, Dt)
+        ref = oracle.coarse_mesh(oproblem(n), u0, step0, steps, Dt)
+        assert rel(out, ref) <= TOL, (n, step0, steps)
+        u = dev(u0)
+        pr.pr_coarse_mesh(g, u, u, step0, steps, Dt)
+        assert torch.equal(u, out)
+    with pytest.raises(pr.PrError):
+        pr.pr_coarse_mesh(grid(10), dev(random_field(10, 1)), torch.empty((10,) * 3, dtype=torch.float64,
+                                                                           device="cuda"), 0, 1, Dt)
+
+
+@pytest.mark.parametrize("K", [0, 2, 4])
+def test_parareal_coarse_mesh_vs_oracle(K):
+    """Alg.1 with G = G_c (PR_FLAG_G_HALF_MESH) against the oracle; K = N_p is exact."""
+    n, Np, nc, nf = 32, 4, 8, 32
+    p = oproblem(n, T=0.01)
+    u0 = random_field(n, 51)
+    uf = oracle.serial_fine(p, Np * nf, u0)
+    ref = oracle.parareal(p, Np, nc, nf, K, u0, uf, g_half_mesh=True)
+    g = grid(n, T=0.01)
+    uT = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+    d = pr.pr_parareal(g, pr.PararealCfg(Np, nc, nf, K, flags=pr.PR_FLAG_G_HALF_MESH), dev(u0), uT,
+                       dev(uf))
+    assert rel(uT, ref.u_T) <= TOL
+    assert np.max(np.abs(np.array(d) - ref.defects)) <= 1e-10
