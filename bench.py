@@ -173,7 +173,7 @@ def cpu_baseline_sample(cfg, target_s=12.0):
     t0 = time.perf_counter()
     u = oracle.fine(p, u, 0, 1, dt)
     t1 = time.perf_counter() - t0
-    steps = max(1, min(16, int(target_s / max(t1, 1e-3))))
+    steps = max(1, min(64, int(target_s / max(t1, 1e-3))))
     t0 = time.perf_counter()
     oracle.fine(p, u, 1, steps, dt)
     el = time.perf_counter() - t0
