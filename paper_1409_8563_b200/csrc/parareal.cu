@@ -1070,6 +1070,7 @@ pr_status pr_comm_init(pr_grid *g, int32_t world, int32_t rank, const void *id) 
     if (!g->comm_stream) CK(cudaStreamCreateWithFlags(&g->comm_stream, cudaStreamNonBlocking));
     g->world = world;
     g->rank = rank;
+    g->mapped_gen = -1;  // peer mappings belong to the previous communicator
     return PR_OK;
 }
 
