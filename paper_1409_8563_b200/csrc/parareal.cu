@@ -1142,7 +1142,7 @@ static pr_status peer_setup(pr_grid *g, double *mail_even, double *mail_odd) {
     g->mapped_gen = -1;
     if (!stream_wait_fn()) return fail(PR_ECUDA, "cuStreamWaitValue32 entry point not found");
     const int W = g->world, r = g->rank;
-    constexpr size_t REC = 3 * sizeof(cudaIpcMemHandle_t);
+    constexpr size_t HREC = 3 * sizeof(cudaIpcMemHandle_t), REC = HREC + 8;  // + seq_base
     // flag words are zeroed once and never reset: sequence numbers only grow
     // (seq_base advances on every peer-mode call, on every rank alike), so a late
     // store from a peer's previous call can never satisfy a newer wait
@@ -1157,7 +1157,10 @@ static pr_status peer_setup(pr_grid *g, double *mail_even, double *mail_odd) {
     CK(cudaIpcGetMemHandle(&h[0], mail_even));
     CK(cudaIpcGetMemHandle(&h[1], mail_odd));
     CK(cudaIpcGetMemHandle(&h[2], g->d_flags));
-    CK(cudaMemcpy(g->d_ipc + REC * size_t(r), h, REC, cudaMemcpyHostToDevice));
+    unsigned char rec[REC] = {};
+    std::memcpy(rec, h, HREC);
+    std::memcpy(rec + HREC, &g->seq_base, sizeof g->seq_base);
+    CK(cudaMemcpy(g->d_ipc + REC * size_t(r), rec, REC, cudaMemcpyHostToDevice));
     NCK(ncclAllGather(g->d_ipc + REC * size_t(r), g->d_ipc, REC, ncclUint8, g->comm, g->comm_stream), -1);
     CK(cudaStreamSynchronize(g->comm_stream));
     std::vector<unsigned char> all(REC * size_t(W));
@@ -1178,6 +1181,13 @@ static pr_status peer_setup(pr_grid *g, double *mail_even, double *mail_odd) {
     if (r > 0) {
         CKS(open(r - 1, 2, &p));
         g->pred_flags = static_cast<unsigned int *>(p);
+    }
+    // common sequence base: the largest any rank has used (grids with different call
+    // histories meet in one communicator); every stale flag value is below it
+    for (int q = 0; q < W; ++q) {
+        unsigned int b = 0;
+        std::memcpy(&b, all.data() + REC * size_t(q) + HREC, sizeof b);
+        g->seq_base = std::max(g->seq_base, b);
     }
     g->mapped_gen = g->pool_gen;
     return PR_OK;
