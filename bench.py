@@ -233,6 +233,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--nu-mode", type=int, default=None)
+    ap.add_argument("--Nt", type=int, default=None, help="override N_t (ratio sweeps, BASELINE configs[4])")
+    ap.add_argument("--NC", type=int, default=None, help="override N_C")
     ap.add_argument("--tol", type=float, default=0.0,
                     help="convergence-controlled stopping tolerance (DESIGN.md C23); 0 = fixed K")
     args = ap.parse_args()
@@ -243,6 +245,9 @@ def main():
     cfg = CONFIGS[args.config]
     if args.nu_mode is not None:
         cfg = cfg.with_(nu_mode=args.nu_mode)
+    if args.Nt is not None or args.NC is not None:
+        cfg = cfg.with_(Nt=args.Nt or cfg.Nt, NC=args.NC or cfg.NC,
+                        name=f"{cfg.name}[Nt={args.Nt or cfg.Nt},NC={args.NC or cfg.NC}]")
     if args.impl == "reference":
         return run_reference(args, cfg)
 
