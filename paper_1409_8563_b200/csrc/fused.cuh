@@ -432,6 +432,17 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
 #pragma unroll
             for (int r = 0; r < RPT + 4; ++r)
                 col[r] = (r >= 2 && r < RPT + 2) ? q[r - 2][(P + 2) % 5] : lds2(ys + (r - 2) * IW);
+            // K_B: u on the ring is in shared memory already; load it before the
+            // stencil so its latency hides under the FMAs
+            const double *au = aring + size_t(p4.slot) * C::AUX_ELEMS;  // aux j
+            const bool outp = j >= 2 && j < w.nz + 2;
+            double2 ubv[KB == K_B ? RPT : 1];
+            if constexpr (KB == K_B) {
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) ubv[r] = lds2(au + sZ + r * EW);
+            } else {
+                (void)au;
+            }
             double2 k[RPT];
 #pragma unroll
             for (int r = 0; r < RPT; ++r)
@@ -439,8 +450,6 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                                      col[r + 1], col[r + 3], col[r + 4], q[r]);
             if (zpos.round > 0) mbar_wait(&empty[zpos.slot], (zpos.round - 1) & 1);
             double *zs = zring + size_t(zpos.slot) * ZS;
-            const double *au = aring + size_t(p4.slot) * C::AUX_ELEMS;  // aux j
-            const bool outp = j >= 2 && j < w.nz + 2;
             if (valid) {
 #pragma unroll
                 for (int r = 0; r < RPT; ++r) {
@@ -450,7 +459,7 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                         z.x = yc.x + (dt / 2.0) * k[r].x;
                         z.y = yc.y + (dt / 2.0) * k[r].y;
                     } else {
-                        const double2 ub = lds2(au + sZ + r * EW);
+                        const double2 ub = ubv[KB == K_B ? r : 0];
                         z.x = ub.x + dt * k[r].x;
                         z.y = ub.y + dt * k[r].y;
                     }
