@@ -448,6 +448,16 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
             for (int r = 0; r < RPT; ++r)
                 k[r] = apply_pair<P>(W, lds2(ys + r * IW - 2), lds2(ys + r * IW + 2), col[r],
                                      col[r + 1], col[r + 3], col[r + 4], q[r]);
+            // K_B: the acc values of this lane's tile points, read before the ring wait
+            double2 acv[KB == K_B ? RPT : 1];
+            if constexpr (KB == K_B) {
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {  // lanes without a tile point read entry 0
+                    const int er = r0 + r;
+                    const bool need = tcol && er >= 2 && er < C::TYO + 2;
+                    acv[r] = lds2(au + C::Z_ELEMS + (need ? tp0 + r * TXO : 0));
+                }
+            }
             if (zpos.round > 0) mbar_wait(&empty[zpos.slot], (zpos.round - 1) & 1);
             double *zs = zring + size_t(zpos.slot) * ZS;
             if (valid) {
@@ -474,7 +484,7 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                             sts2(zs + C::Z_ELEMS + tp, t0);
                             sts2(zs + C::Z_ELEMS + C::T_ELEMS + tp, yc);
                         } else {
-                            const double2 ac = lds2(au + C::Z_ELEMS + tp);
+                            const double2 ac = acv[KB == K_B ? r : 0];
                             double2 t0;
                             t0.x = ac.x + (dt / 3.0) * k[r].x;
                             t0.y = ac.y + (dt / 3.0) * k[r].y;
