@@ -202,7 +202,7 @@ using FusedP1 = FusedCfgP<16, 9, 4, 2, 2, 1>;
 using FusedP2 = FusedCfgP<16, 8, 5, 2, 2, 2>;   // 5-slot intermediate ring
 using FusedP3 = FusedCfgP<16, 9, 4, 2, 2, 2>;     // two producer warps, cp.async only
 using FusedP4 = FusedCfgP<16, 9, 4, 2, 2, 2, 2>;  // + TMA tensor fills (default, PR_FTILE=14)
-using FusedP5 = FusedCfgP<16, 9, 4, 2, 2, 1, 2>;
+using FusedP5 = FusedCfgP<16, 9, 5, 2, 2, 2, 2>;  // + 5-slot intermediate ring
 using FusedP6 = FusedCfgP<16, 8, 4, 2, 2, 2>;
 using FusedP7 = FusedCfgP<16, 8, 4, 2, 2, 2, 2>;
 using FusedP8 = FusedCfgP<16, 9, 4, 4, 4, 2, 2>;  // four rows per lane (7 warps: <= 256 threads at ~190 regs)
