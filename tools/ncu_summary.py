@@ -14,20 +14,27 @@ STALLS = ["barrier", "long_scoreboard", "short_scoreboard", "wait", "mio_throttl
           "math_pipe_throttle", "selected", "not_selected", "no_instruction", "drain", "branch_resolving"]
 
 
+SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6}
+
+
 def rows(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(out.splitlines()))
-    return r[0], r[2:]
+    return r[0], r[1], r[2:]
 
 
 def main(rep):
-    hdr, data = rows(rep)
+    hdr, units, data = rows(rep)
     for r in data:
         name = r[hdr.index("Kernel Name")]
         parts = [name[:40]]
         for m, short in WANT:
             if m in hdr:
-                parts.append(f"{short}={r[hdr.index(m)]}")
+                i = hdr.index(m)
+                v = r[i]
+                if units[i] in SCALE:  # byte counters reported in MB whatever ncu's unit
+                    v = f"{float(v.replace(',', '')) * SCALE[units[i]]:.3f}"
+                parts.append(f"{short}={v}")
         st = []
         for s in STALLS:
             m = f"smsp__average_warps_issue_stalled_{s}_per_issue_active.ratio"
