@@ -175,6 +175,7 @@ struct FusedCfgP {
     static constexpr int FILL = FILL_;
     static constexpr int RPTA = RPTA_, RPT = RPTB_;
     static constexpr int EW = TXO + 4, EH = TYO + 4, IW = TXO + 8, IH = TYO + 8;
+    static constexpr int HX = 4, HY = 4, HZ = 4;  // input halo (two radius-2 stages)
     static constexpr int IWS = IW + 2, EWS = EW + 6;  // padded pitches: no bank conflicts for the lane maps
     static constexpr int GA = EH / RPTA, GB = TYO / RPT;
     static constexpr int A_ITEMS = (EW / 2) * GA, B_ITEMS = (TXO / 2) * GB;
@@ -273,7 +274,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const WorkItem w = decode_item(a, item, TXO, C::TYO);
-        const int E = w.nz + 8, NJ = w.nz + 4;
+        const int E = w.nz + 2 * C::HZ, NJ = w.nz + 4;
         int ysrc[NY], ydst[NY];
 #pragma unroll
         for (int k = 0; k < NY; ++k) {
@@ -282,8 +283,8 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
             ydst[k] = 0;
             if (c < C::Y_CHUNKS) {
                 int r, cc;
-                line_order(c, C::IH, TXO / 2, 2, r, cc);
-                ysrc[k] = wrap1(w.y0 - 4 + r, n) * n + wrap1(w.x0 - 4 + 2 * cc, n);
+                line_order(c, C::IH, TXO / 2, C::HX / 2, r, cc);
+                ysrc[k] = wrap1(w.y0 - C::HY + r, n) * n + wrap1(w.x0 - C::HX + 2 * cc, n);
                 ydst[k] = 8 * (r * IW + 2 * cc);
             }
         }
@@ -315,9 +316,10 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
             }
         }
         // TMA fills for tiles whose boxes stay inside the field (no periodic seam)
-        const bool tma = C::FILL == 2 && w.x0 >= TXO && w.x0 + 2 * TXO <= n && w.y0 >= 4 &&
-                         w.y0 + C::TYO + 4 <= n;
-        int zin = wrap1(w.z_begin - 4, n);
+        const bool tma = C::FILL == 2 && w.x0 >= C::HX && w.x0 - C::HX + IW <= n &&
+                         w.y0 >= C::HY && w.y0 - C::HY + C::IH <= n &&
+                         (KB == K_A || w.x0 - 2 + EW <= n);
+        int zin = wrap1(w.z_begin - C::HZ, n);
 #pragma unroll 1
         for (int e = 0; e < E; ++e) {
             if (pos.round > 0) mbar_wait(&in_empty[pos.slot], (pos.round - 1) & 1);
@@ -330,8 +332,8 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
                         const bool ca = ua && j >= 2 && j < w.nz + 2;
                         mbar_expect_tx(bar, 8u * (C::IH * IW + (ua ? C::EH * EW : 0) +
                                                   (ca ? C::T_ELEMS : 0)));
-                        tma_load3(yring_s + uint32_t(pos.slot) * (C::Y_ELEMS * 8), &tm->y, w.x0 - 4,
-                                  w.y0 - 4, zin, bar);
+                        tma_load3(yring_s + uint32_t(pos.slot) * (C::Y_ELEMS * 8), &tm->y,
+                                  w.x0 - C::HX, w.y0 - C::HY, zin, bar);
                         if (ua) {
                             const int zaux = zin >= 2 ? zin - 2 : zin - 2 + n;
                             const uint32_t dst = aring_s + uint32_t(pos.slot) * (C::AUX_ELEMS * 8);
@@ -585,6 +587,162 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
         zc_pos.step(ZD);
         mbar_arrive(&empty[zc_pos.slot]);
     }
+}
+
+// ---------------------------------------------------------------------------
+// G (one forward-Euler step, Alg.2) in the same persistent,
+// warp-specialised form: producer warps stream input planes with a (2, 1, 1)
+// halo (TMA tensor copies for tiles away from the seams, cp.async otherwise)
+// into a DEPTH-slot ring; consumer lanes own two adjacent x points and RPT
+// rows, keep z neighbours in a 3-deep register queue and write
+// u' = u + Dt L_G(u) straight to HBM.  Same per-point operation order as
+// stencil_kernel<K_COARSE> (bitwise identical results).
+template <int TYO_, int DEPTH_, int RPT_, int PW_, int FILL_>
+struct CoarseCfgP {
+    static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, RPT = RPT_, PW = PW_, FILL = FILL_;
+    static constexpr int HX = 2, HY = 1, HZ = 1;  // radius-1 stencil; x halo pair-aligned
+    static constexpr int IW = TXO + 2 * HX, IH = TYO + 2 * HY, IWS = IW;
+    static constexpr int Y_ELEMS = (IH * IWS + 15) / 16 * 16;  // 128-byte aligned slots (TMA)
+    static constexpr int Y_CHUNKS = IH * (IW / 2);
+    static constexpr int GC = TYO / RPT, C_ITEMS = (TXO / 2) * GC;
+    static constexpr int NTA = (C_ITEMS + 31) / 32 * 32, NTB = 0, NTP = 32 * PW, NT = NTA + NTP;
+    static constexpr int MAXR = (65536 / NT) / 8 * 8 > 255 ? 255 : (65536 / NT) / 8 * 8;
+    // unused by the K_A producer path (aux planes belong to the RK4 K_B kernel)
+    static constexpr int EW = IW, EH = IH, EWS = IWS, Z_ELEMS = 0, T_ELEMS = 0, AUX_ELEMS = 0,
+                         U_CHUNKS = 0, C_CHUNKS = 0, AD = 0, ZD = 1, RPTA = RPT;
+    static_assert(TYO % RPT == 0 && C_ITEMS % 32 == 0, "full consumer warps");
+    static size_t smem_bytes() { return sizeof(double) * size_t(DEPTH) * Y_ELEMS; }
+};
+using CoarseP0 = CoarseCfgP<16, 8, 2, 2, 2>;   // default
+using CoarseP1 = CoarseCfgP<16, 8, 1, 2, 2>;   // one row per lane (8 consumer warps)
+using CoarseP2 = CoarseCfgP<16, 10, 2, 1, 2>;
+
+template <class Body>
+__device__ __forceinline__ void rotating_loop3(int NJ, Body &&body) {
+    int j = 0;
+#pragma unroll 1
+    for (; j + 3 <= NJ; j += 3) {
+        body(Ph<0>{}, j);
+        body(Ph<1>{}, j + 1);
+        body(Ph<2>{}, j + 2);
+    }
+    if (j < NJ) body(Ph<0>{}, j++);
+    if (j < NJ) body(Ph<1>{}, j++);
+}
+
+template <class C>
+__device__ __forceinline__ void stage_c_p(const StencilArgs &a, double *sm, int items,
+                                          uint64_t *in_full, uint64_t *in_empty) {
+    constexpr int RPT = C::RPT, IW = C::IWS, TXO = C::TXO, DEPTH = C::DEPTH;
+    const double *yring = sm;
+    const int n = a.n;
+    const size_t nn = size_t(n) * n;
+    const int t = threadIdx.x;
+    const int m = t % (TXO / 2), g = t / (TXO / 2);
+    const int r0 = g * RPT;
+    const int sY = (r0 + C::HY) * IW + 2 * m + C::HX;
+
+    // folded weights of Alg.2 (same expressions as stencil_kernel<K_COARSE>)
+    const double nu = a.nu_tab[*a.nu_pos + a.j_local];
+    const double al = nu * a.inv_dx * a.inv_dx;
+    double w0 = -6.0 * al, wm1[3], wp1[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const double b1 = a.c[d] * a.inv_dx;
+        if (a.c[d] > 0) {
+            wm1[d] = al + b1; wp1[d] = al; w0 -= b1;
+        } else {
+            wm1[d] = al; wp1[d] = al - b1; w0 += b1;
+        }
+    }
+    const double dt = a.dt;
+
+    RingPos base;  // input element 0 of the current item
+#pragma unroll 1
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const WorkItem w = decode_item(a, item, TXO, C::TYO);
+        double *o0 = a.o0 + size_t(w.z_begin) * nn + size_t(w.y0 + r0) * n + w.x0 + 2 * m;
+        double2 q[RPT][3];
+        RingPos p0 = base;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            mbar_wait(&in_full[p0.slot], p0.round & 1);
+            const double *ys = yring + size_t(p0.slot) * C::Y_ELEMS + sY;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) q[r][e] = lds2(ys + r * IW);
+            p0.step(DEPTH);
+        }
+        mbar_arrive(&in_empty[base.slot]);      // element 0: queue only
+        RingPos pc = ring_at(base, 1, DEPTH), pq = p0;  // elements j+1 (centre), j+2
+        rotating_loop3(w.nz, [&](auto ph, int j) {
+            constexpr int P = decltype(ph)::value;  // q[.][P] = z-1, [P+1] = z, [P+2] = z+1
+            mbar_wait(&in_full[pq.slot], pq.round & 1);
+            const double *yq = yring + size_t(pq.slot) * C::Y_ELEMS + sY;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) q[r][(P + 2) % 3] = lds2(yq + r * IW);
+            const double *ys = yring + size_t(pc.slot) * C::Y_ELEMS + sY;
+            double2 col[RPT + 2];
+#pragma unroll
+            for (int r = 0; r < RPT + 2; ++r)
+                col[r] = (r >= 1 && r <= RPT) ? q[r - 1][(P + 1) % 3] : lds2(ys + (r - 1) * IW);
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                const double2 L = lds2(ys + r * IW - 2), R = lds2(ys + r * IW + 2);
+                const double2 c = q[r][(P + 1) % 3], zm = q[r][P % 3], zp = q[r][(P + 2) % 3];
+                double2 v;
+                {
+                    double ax = wm1[0] * L.y;
+                    ax = fma(wp1[0], c.y, ax);
+                    double ay = wm1[1] * col[r].x;
+                    ay = fma(wp1[1], col[r + 2].x, ay);
+                    double az = wm1[2] * zm.x;
+                    az = fma(wp1[2], zp.x, az);
+                    const double Lv = fma(w0, c.x, ax) + (ay + az);
+                    v.x = c.x + dt * Lv;
+                }
+                {
+                    double ax = wm1[0] * c.x;
+                    ax = fma(wp1[0], R.x, ax);
+                    double ay = wm1[1] * col[r].y;
+                    ay = fma(wp1[1], col[r + 2].y, ay);
+                    double az = wm1[2] * zm.y;
+                    az = fma(wp1[2], zp.y, az);
+                    const double Lv = fma(w0, c.y, ax) + (ay + az);
+                    v.y = c.y + dt * Lv;
+                }
+                *reinterpret_cast<double2 *>(o0 + size_t(r) * n) = v;
+            }
+            o0 += nn;
+            mbar_arrive(&in_empty[pc.slot]);  // the centre plane is no longer read from smem
+            pc.step(DEPTH);
+            pq.step(DEPTH);
+        });
+        mbar_arrive(&in_empty[pc.slot]);  // the item's last element (queue only)
+        base = ring_at(pc, 1, DEPTH);
+    }
+}
+
+template <class C>
+__global__ void __maxnreg__(C::MAXR)
+coarse_persist_kernel(const StencilArgs a, const __grid_constant__ TmaMaps tm) {
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) uint64_t in_full[C::DEPTH], in_empty[C::DEPTH];
+    const int items = a.tiles_x * a.tiles_y * a.chunks_z;
+    if constexpr (C::FILL == 2) {
+        if (smem_u32(sm) & 127) __trap();
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::DEPTH; ++s) {
+            mbar_init(&in_full[s], C::NTP);
+            mbar_init(&in_empty[s], C::NTA);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x < C::NTA)
+        stage_c_p<C>(a, sm, items, in_full, in_empty);
+    else
+        producer_p<K_A, C>(a, &tm, sm, items, in_full, in_empty);
 }
 
 template <int KB, class C>

@@ -88,6 +88,9 @@ struct pr_grid {
     int variant = 0;                    // stencil tile variant (PR_TILE env, tuning)
     bool f2 = false;                    // fused two-kernel RK4 step (tile-aligned n)
     int fvariant = 14;                  // fused tile variant (PR_FTILE env 10..19, tuning)
+    bool c2 = false;                    // persistent TMA-fed G kernel (n % 32 == 0; PR_C2=0 disables)
+    int cvariant = 0;                   // its variant (PR_CTILE 0..2)
+    LaunchCfg lcp;                      // its launch config
     LaunchCfg lf[2];                    // launch configs of fused_persist_kernel<K_A>, <K_B>
     pr_problem prob{};
     int n = 0;
@@ -285,6 +288,57 @@ static pr_status setup_fused_persist(pr_grid *g) {
     return PR_OK;
 }
 
+template <class C>
+static pr_status setup_coarse_persist(pr_grid *g) {
+    const size_t smem = C::smem_bytes();
+    CK(cudaFuncSetAttribute(coarse_persist_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(smem)));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, coarse_persist_kernel<C>, C::NT, smem));
+    if (occ < 1) return fail(PR_ECUDA, "persistent coarse kernel cannot be resident");
+    LaunchCfg &c = g->lcp;
+    const int n = g->n;
+    c.occ = occ;
+    c.threads = C::NT;
+    c.smem = smem;
+    c.tiles_x = n / C::TXO;
+    c.tiles_y = n / C::TYO;
+    const int slots = g->sms * occ;
+    const int ch = pick_chunks(n, c.tiles_x * c.tiles_y, slots, 1);
+    c.cz = (n + ch - 1) / ch;
+    c.chunks_z = (n + c.cz - 1) / c.cz;
+    c.blocks = std::min(c.tiles_x * c.tiles_y * c.chunks_z, slots);
+    return PR_OK;
+}
+
+static pr_status setup_coarse(pr_grid *g) {
+    switch (g->cvariant) {
+    case 1: return setup_coarse_persist<CoarseP1>(g);
+    case 2: return setup_coarse_persist<CoarseP2>(g);
+    default: return setup_coarse_persist<CoarseP0>(g);
+    }
+}
+
+template <class C>
+static void launch_coarse_persist(pr_grid *g, const StencilArgs &a0, cudaStream_t st) {
+    StencilArgs a = a0;
+    const LaunchCfg &c = g->lcp;
+    a.tiles_x = c.tiles_x;
+    a.tiles_y = c.tiles_y;
+    a.cz = c.cz;
+    a.chunks_z = c.chunks_z;
+    TmaMaps tm;
+    memset(&tm, 0, sizeof tm);
+    if constexpr (C::FILL == 2) {
+        if (!tma_encode3(&tm.y, a.y, g->n, C::IWS, C::IH)) {
+            g->launch_err = fail(PR_ECUDA, "cuTensorMapEncodeTiled failed (coarse kernel)");
+            return;
+        }
+    }
+    coarse_persist_kernel<C><<<c.blocks, c.threads, c.smem, st>>>(a, tm);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 template <int KB>
 static pr_status setup_fused(pr_grid *g) {
     switch (g->fvariant) {
@@ -423,7 +477,15 @@ static void enqueue_coarse_step(pr_grid *g, const double *src, double *dst, int 
     a.dt = dt;
     a.y = src;
     a.o0 = dst;
-    launch_stencil<K_COARSE>(g, a, st);
+    if (g->c2) {
+        switch (g->cvariant) {
+        case 1: launch_coarse_persist<CoarseP1>(g, a, st); break;
+        case 2: launch_coarse_persist<CoarseP2>(g, a, st); break;
+        default: launch_coarse_persist<CoarseP0>(g, a, st); break;
+        }
+    } else {
+        launch_stencil<K_COARSE>(g, a, st);
+    }
 }
 
 static pr_status set_pos(pr_grid *g, int which, long long v, cudaStream_t st) {
@@ -679,6 +741,11 @@ static pr_status run_coarse(pr_grid *g, const double *uin, double *uout, int64_t
         ++done;
     }
     CKL();
+    if (g->launch_err != PR_OK) {
+        const pr_status e = g->launch_err;
+        g->launch_err = PR_OK;
+        return e;
+    }
     return PR_OK;
 }
 
@@ -803,6 +870,12 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
         if ((s = setup_fused<K_A>(g)) != PR_OK) return bail(s);
         if ((s = setup_fused<K_B>(g)) != PR_OK) return bail(s);
     }
+    {
+        const char *ce = getenv("PR_C2");
+        if (const char *cv = getenv("PR_CTILE")) g->cvariant = std::max(0, std::min(2, atoi(cv)));
+        g->c2 = (n % CoarseP0::TXO == 0) && (n % CoarseP0::TYO == 0) && !(ce && ce[0] == '0');
+    }
+    if (g->c2 && (s = setup_coarse(g)) != PR_OK) return bail(s);
     if ((s = ensure_red(g, 8)) != PR_OK) return bail(s);
     GK(cudaMallocHost(&g->h_flag, 2 * sizeof(double)));
     // generous initial table capacities (graphs capture the pointers)

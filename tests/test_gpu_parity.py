@@ -356,3 +356,21 @@ def test_parareal_coarse_mesh_vs_oracle(K):
                        dev(uf))
     assert rel(uT, ref.u_T) <= TOL
     assert np.max(np.abs(np.array(d) - ref.defects)) <= 1e-10
+
+
+@pytest.mark.parametrize("variant", ["0", "1", "2"])
+@pytest.mark.parametrize("n", [32, 64, 128])
+def test_coarse_kernels_bitwise(n, variant, monkeypatch):
+    """The persistent TMA-fed G kernel (PR_CTILE variants) gives the lockstep
+    stencil_kernel<K_COARSE>'s bits (same per-point operation order)."""
+    u0 = dev(random_field(n, 52))
+    outs = []
+    for c2 in ("0", "1"):
+        monkeypatch.setenv("PR_C2", c2)
+        monkeypatch.setenv("PR_CTILE", variant)
+        g = pr.Grid(pr.Problem(n, c=PARITY_C))
+        out = torch.empty_like(u0)
+        pr.pr_coarse(g, u0, out, 5, 37, 4e-4 * (32 / n) ** 2)
+        outs.append(out)
+        g.destroy()
+    assert torch.equal(outs[0], outs[1])

@@ -17,10 +17,19 @@ ref = None
 u0 = None
 for ch in chunks:
     for v in variants:
-        # "f2" = fused two-kernel RK4 step; "0".."3" = four-stage tile variants
-        os.environ["PR_F2"] = "1" if v.startswith("f2") else "0"
-        os.environ["PR_FTILE"] = v[3:] if v.startswith("f2_") else "0"
-        os.environ["PR_TILE"] = "0" if v.startswith("f2") else str(v)
+        # "f2_N" = fused two-kernel RK4 step, variant N; "0".."3" = four-stage tile variants;
+        # "cN" = default F with persistent coarse variant N; "cold" = the lockstep coarse kernel
+        if v.startswith("c"):
+            os.environ["PR_F2"] = "1"
+            os.environ["PR_FTILE"] = "14"
+            os.environ["PR_TILE"] = "0"
+            os.environ["PR_C2"] = "0" if v == "cold" else "1"
+            os.environ["PR_CTILE"] = "0" if v == "cold" else v[1:]
+        else:
+            os.environ.pop("PR_C2", None)
+            os.environ["PR_F2"] = "1" if v.startswith("f2") else "0"
+            os.environ["PR_FTILE"] = v[3:] if v.startswith("f2_") else "14"
+            os.environ["PR_TILE"] = "0" if v.startswith("f2") else str(v)
         if ch is None:
             os.environ.pop("PR_CHUNKS_Z", None)
         else:
