@@ -396,6 +396,15 @@ def main():
                "algorithmic_bytes_per_launch": 128 * n ** 3, "launch_ms": t4,
                "note": "alternative F path (PR_F2=0), timed on a separate grid after the timed region"}
 
+    # G's own roofline: 16 B per point per Euler step at the measured tau_c
+    roof_g = None
+    if tc_all > 0 and args.g_mesh == "full":
+        ag = 16 * n ** 3 / (tc_all / 1e3) / 1e9
+        roof_g = {"bound": "hbm", "achieved": ag, "peak": peak, "unit": "GB/s", "frac": ag / peak,
+                  "kernel": "coarse_persist_kernel: one Euler step of G (TMA-fed, persistent)",
+                  "algorithmic_bytes_per_launch": 16 * n ** 3, "launch_ms": tc_all,
+                  "note": "tau_c of the serial G run on the last rank (outside the timed region)"}
+
     # e2e: the same solve through the public API with host buffers (pinned), copies timed
     e2e = None
     if not args.no_e2e:
@@ -477,6 +486,7 @@ def main():
                          "launch_ms": t_fine_step_ms, "peak_source": peak_src,
                          "point_steps_per_s": n ** 3 / (t_fine_step_ms / 1e3)},
             "roofline_four_stage": alt,
+            "roofline_coarse": roof_g,
             "gpu_launches": int(launches),
             "clocks": clocks,
         }
