@@ -181,8 +181,13 @@ struct FusedCfgP {
     static constexpr int A_ITEMS = (EW / 2) * GA, B_ITEMS = (TXO / 2) * GB;
     static constexpr int WA = (A_ITEMS + 31) / 32, WB = (B_ITEMS + 31) / 32;
     static constexpr int NTA = 32 * WA, NTB = 32 * WB, NTP = 32 * PW, NT = NTA + NTB + NTP;
-    // register cap: the whole register file for one CTA of NT threads (multiple of 8)
+    // register cap: the whole register file for one CTA of NT threads (multiple of 8),
+    // or PRK_FUSED_MAXR when the build defines it (tuning)
+#ifdef PRK_FUSED_MAXR
+    static constexpr int MAXR = PRK_FUSED_MAXR;
+#else
     static constexpr int MAXR = (65536 / NT) / 8 * 8 > 255 ? 255 : (65536 / NT) / 8 * 8;
+#endif
     static constexpr int AD = DEPTH;  // aux slots follow the input slots
     // Z_ELEMS padded to 16 doubles: every slot and its T part stay 128-byte aligned (TMA)
     static constexpr int Y_ELEMS = IH * IWS, Z_ELEMS = (EH * EWS + 15) / 16 * 16, T_ELEMS = TYO * TXO;
