@@ -166,13 +166,18 @@ __device__ __forceinline__ double2 apply_pair(const Weights &W, double2 L, doubl
 // items, so the producer warp streams the next item's first planes while the
 // compute warps finish the current one (no per-item pipeline fill).  Aux planes
 // (K_B) share the slot index of the input element they ride with.
-template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_, int PW_ = 1, int FILL_ = 0>
+template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_, int PW_ = 1, int FILL_ = 0,
+          int UIN_ = 0>
 struct FusedCfgP {
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = 1, XP = 2,
                          PROD = 1, PW = PW_;  // PW producer warps
     // FILL 0: every plane by 16-byte cp.async; 2: planes of tiles away from the
     // periodic seams by one TMA tensor copy per array (box = padded slot rows)
     static constexpr int FILL = FILL_;
+    // UIN: K_A's stage B reads u (for Yb = u + dt/2 k2) from the input ring instead of a
+    // copy stage A leaves in the intermediate ring; input slots are then released by both
+    // stages (one fewer shared store per point, slots held two planes longer)
+    static constexpr int UIN = UIN_;
     static constexpr int RPTA = RPTA_, RPT = RPTB_;
     static constexpr int EW = TXO + 4, EH = TYO + 4, IW = TXO + 8, IH = TYO + 8;
     static constexpr int HX = 4, HY = 4, HZ = 4;  // input halo (two radius-2 stages)
@@ -196,7 +201,8 @@ struct FusedCfgP {
     static_assert(TYO % RPT == 0 && EH % RPTA == 0, "rows must split into row groups");
     static_assert(Y_ELEMS % 16 == 0 && Z_ELEMS % 16 == 0, "slots must stay 128-byte aligned");
     static_assert(DEPTH >= 5 && ZD >= 3, "rings too shallow");
-    template <int KB> static constexpr int NTV = KB == K_A ? 2 : 1;
+    template <int KB> static constexpr int NTV = (KB == K_A && !UIN) ? 2 : 1;
+    template <int KB> static constexpr int IN_CONSUMERS = (KB == K_A && UIN) ? NTA + NTB : NTA;
     template <int KB> static constexpr int ZS_ELEMS = Z_ELEMS + NTV<KB> * T_ELEMS;
     template <int KB> static constexpr size_t smem_bytes() {
         return sizeof(double) * (size_t(DEPTH) * Y_ELEMS + (KB == K_B ? size_t(AD) * AUX_ELEMS : 0) +
@@ -209,7 +215,7 @@ using FusedP2 = FusedCfgP<16, 8, 5, 2, 2, 2>;   // 5-slot intermediate ring
 using FusedP3 = FusedCfgP<16, 9, 4, 2, 2, 2>;     // two producer warps, cp.async only
 using FusedP4 = FusedCfgP<16, 9, 4, 2, 2, 2, 2>;  // + TMA tensor fills (default, PR_FTILE=14)
 using FusedP5 = FusedCfgP<16, 9, 5, 2, 2, 2, 2>;  // + 5-slot intermediate ring
-using FusedP6 = FusedCfgP<16, 8, 4, 2, 2, 2>;
+using FusedP6 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 1>;  // + K_A stage B reads u from the input ring
 using FusedP7 = FusedCfgP<16, 8, 4, 2, 2, 2, 2>;
 using FusedP8 = FusedCfgP<16, 9, 4, 4, 4, 2, 2>;  // four rows per lane (7 warps: <= 256 threads at ~190 regs)
 using FusedP9 = FusedCfgP<16, 9, 4, 4, 4, 1, 2>;
@@ -489,7 +495,7 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                             t0.x = yc.x + (dt / 6.0) * k[r].x;
                             t0.y = yc.y + (dt / 6.0) * k[r].y;
                             sts2(zs + C::Z_ELEMS + tp, t0);
-                            sts2(zs + C::Z_ELEMS + C::T_ELEMS + tp, yc);
+                            if constexpr (!C::UIN) sts2(zs + C::Z_ELEMS + C::T_ELEMS + tp, yc);
                         } else {
                             const double2 ac = acv[KB == K_B ? r : 0];
                             double2 t0;
@@ -515,7 +521,8 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
 
 template <int KB, class C>
 __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int items,
-                                          uint64_t *full, uint64_t *empty) {
+                                          uint64_t *full, uint64_t *empty, uint64_t *in_empty) {
+    constexpr bool UIN = KB == K_A && C::UIN;
     constexpr int RPT = C::RPT, EW = C::EWS, TXO = C::TXO, ZD = C::ZD, DEPTH = C::DEPTH;
     constexpr int ZS = C::template ZS_ELEMS<KB>;
     double *zring = sm + size_t(DEPTH) * C::Y_ELEMS + (KB == K_B ? size_t(C::AD) * C::AUX_ELEMS : 0);
@@ -527,6 +534,8 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
     const int r0 = g * RPT;
     const int sZ = (r0 + 2) * EW + 2 * m + 2;
     const int sT = r0 * TXO + 2 * m;
+    const double *yring = sm;
+    const int sU = (r0 + C::HY) * C::IWS + 2 * m + C::HX;  // tile point in an input slot
 
     const long long row = (*a.nu_pos + a.j_local) * 4;
     Weights W;
@@ -534,6 +543,7 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
     const double dt = a.dt;
 
     RingPos zq_pos;  // Z plane j of the current item
+    RingPos in_pos;  // UIN: input element j of the current item
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const WorkItem w = decode_item(a, item, TXO, C::TYO);
@@ -563,7 +573,10 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
                     const size_t gofs = size_t(r) * n;
                     if (KB == K_A) {
                         const double2 t0 = lds2(zs + C::Z_ELEMS + sT + r * TXO);
-                        const double2 t1 = lds2(zs + C::Z_ELEMS + C::T_ELEMS + sT + r * TXO);
+                        // u at the output point: input element j (plane z_begin + j - 4)
+                        const double2 t1 =
+                            UIN ? lds2(yring + size_t(in_pos.slot) * C::Y_ELEMS + sU + r * C::IWS)
+                                : lds2(zs + C::Z_ELEMS + C::T_ELEMS + sT + r * TXO);
                         double2 v0, v1;
                         v0.x = t0.x + (dt / 3.0) * kB.x;  v0.y = t0.y + (dt / 3.0) * kB.y;
                         v1.x = t1.x + (dt / 2.0) * kB.x;  v1.y = t1.y + (dt / 2.0) * kB.y;
@@ -586,11 +599,22 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
                 zc_pos.step(ZD);
             }
             zq_pos.step(ZD);
+            if constexpr (UIN) {  // input element j: read above (j >= 4) or never (j < 4)
+                mbar_arrive(&in_empty[in_pos.slot]);
+                in_pos.step(DEPTH);
+            }
         });
         // release the item's last two Z planes (never a centre)
         mbar_arrive(&empty[zc_pos.slot]);
         zc_pos.step(ZD);
         mbar_arrive(&empty[zc_pos.slot]);
+        if constexpr (UIN) {  // input elements nz+4 .. nz+7 (z halo only)
+#pragma unroll 1
+            for (int e = 0; e < 4; ++e) {
+                mbar_arrive(&in_empty[in_pos.slot]);
+                in_pos.step(DEPTH);
+            }
+        }
     }
 }
 
@@ -766,7 +790,7 @@ fused_persist_kernel(const StencilArgs a, const __grid_constant__ TmaMaps tm) {
         }
         for (int s = 0; s < C::DEPTH; ++s) {
             mbar_init(&in_full[s], C::NTP);
-            mbar_init(&in_empty[s], C::NTA);
+            mbar_init(&in_empty[s], C::template IN_CONSUMERS<KB>);
         }
         fence_mbar_init();
     }
@@ -774,7 +798,7 @@ fused_persist_kernel(const StencilArgs a, const __grid_constant__ TmaMaps tm) {
     if (threadIdx.x < C::NTA)
         stage_a_p<KB, C>(a, sm, items, full, empty, in_full, in_empty);
     else if (threadIdx.x < C::NTA + C::NTB)
-        stage_b_p<KB, C>(a, sm, items, full, empty);
+        stage_b_p<KB, C>(a, sm, items, full, empty, in_empty);
     else
         producer_p<KB, C>(a, &tm, sm, items, in_full, in_empty);
 }
