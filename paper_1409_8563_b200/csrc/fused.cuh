@@ -167,7 +167,7 @@ __device__ __forceinline__ double2 apply_pair(const Weights &W, double2 L, doubl
 // compute warps finish the current one (no per-item pipeline fill).  Aux planes
 // (K_B) share the slot index of the input element they ride with.
 template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_, int PW_ = 1, int FILL_ = 0,
-          int UIN_ = 0>
+          int UIN_ = 0, int DEPTHA_ = DEPTH_>
 struct FusedCfgP {
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = 1, XP = 2,
                          PROD = 1, PW = PW_;  // PW producer warps
@@ -201,11 +201,13 @@ struct FusedCfgP {
     static_assert(TYO % RPT == 0 && EH % RPTA == 0, "rows must split into row groups");
     static_assert(Y_ELEMS % 16 == 0 && Z_ELEMS % 16 == 0, "slots must stay 128-byte aligned");
     static_assert(DEPTH >= 5 && ZD >= 3, "rings too shallow");
+    // input ring depth per kernel: K_A has shared memory to spare (no aux ring)
+    template <int KB> static constexpr int DEPTH_K = KB == K_A ? DEPTHA_ : DEPTH;
     template <int KB> static constexpr int NTV = (KB == K_A && !UIN) ? 2 : 1;
     template <int KB> static constexpr int IN_CONSUMERS = (KB == K_A && UIN) ? NTA + NTB : NTA;
     template <int KB> static constexpr int ZS_ELEMS = Z_ELEMS + NTV<KB> * T_ELEMS;
     template <int KB> static constexpr size_t smem_bytes() {
-        return sizeof(double) * (size_t(DEPTH) * Y_ELEMS + (KB == K_B ? size_t(AD) * AUX_ELEMS : 0) +
+        return sizeof(double) * (size_t(DEPTH_K<KB>) * Y_ELEMS + (KB == K_B ? size_t(AD) * AUX_ELEMS : 0) +
                                  size_t(ZD) * ZS_ELEMS<KB>);
     }
 };
@@ -216,9 +218,9 @@ using FusedP3 = FusedCfgP<16, 9, 4, 2, 2, 2>;     // two producer warps, cp.asyn
 using FusedP4 = FusedCfgP<16, 9, 4, 2, 2, 2, 2>;  // + TMA tensor fills (default, PR_FTILE=14)
 using FusedP5 = FusedCfgP<16, 9, 5, 2, 2, 2, 2>;  // + 5-slot intermediate ring
 using FusedP6 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 1>;  // + K_A stage B reads u from the input ring
-using FusedP7 = FusedCfgP<16, 8, 4, 2, 2, 2, 2>;
+using FusedP7 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 12>;  // 12-slot input ring in K_A
 using FusedP8 = FusedCfgP<16, 9, 4, 4, 4, 2, 2>;  // four rows per lane (7 warps: <= 256 threads at ~190 regs)
-using FusedP9 = FusedCfgP<16, 9, 4, 4, 4, 1, 2>;
+using FusedP9 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 1, 13>;  // UIN + 13-slot input ring in K_A
 
 struct WorkItem {
     int x0, y0, z_begin, nz;
@@ -270,7 +272,7 @@ __device__ __forceinline__ void line_order(int c, int rows, int mid, int hc, int
 template <int KB, class C>
 __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *tm, double *sm,
                                            int items, uint64_t *in_full, uint64_t *in_empty) {
-    constexpr int DEPTH = C::DEPTH, EW = C::EWS, IW = C::IWS, TXO = C::TXO;
+    constexpr int DEPTH = C::template DEPTH_K<KB>, EW = C::EWS, IW = C::IWS, TXO = C::TXO;
     constexpr int NP = C::NTP;
     constexpr int NY = (C::Y_CHUNKS + NP - 1) / NP, NU = (C::U_CHUNKS + NP - 1) / NP,
                   NC = (C::C_CHUNKS + NP - 1) / NP;
@@ -394,7 +396,7 @@ template <int KB, class C>
 __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int items,
                                           uint64_t *full, uint64_t *empty, uint64_t *in_full,
                                           uint64_t *in_empty) {
-    constexpr int RPT = C::RPTA, DEPTH = C::DEPTH, EW = C::EWS, IW = C::IWS, TXO = C::TXO,
+    constexpr int RPT = C::RPTA, DEPTH = C::template DEPTH_K<KB>, EW = C::EWS, IW = C::IWS, TXO = C::TXO,
                   ZD = C::ZD;
     constexpr int ZS = C::template ZS_ELEMS<KB>;
     double *yring = sm;
@@ -523,7 +525,7 @@ template <int KB, class C>
 __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int items,
                                           uint64_t *full, uint64_t *empty, uint64_t *in_empty) {
     constexpr bool UIN = KB == K_A && C::UIN;
-    constexpr int RPT = C::RPT, EW = C::EWS, TXO = C::TXO, ZD = C::ZD, DEPTH = C::DEPTH;
+    constexpr int RPT = C::RPT, EW = C::EWS, TXO = C::TXO, ZD = C::ZD, DEPTH = C::template DEPTH_K<KB>;
     constexpr int ZS = C::template ZS_ELEMS<KB>;
     double *zring = sm + size_t(DEPTH) * C::Y_ELEMS + (KB == K_B ? size_t(C::AD) * C::AUX_ELEMS : 0);
     const int n = a.n;
@@ -640,6 +642,7 @@ struct CoarseCfgP {
     static constexpr int EW = IW, EH = IH, EWS = IWS, Z_ELEMS = 0, T_ELEMS = 0, AUX_ELEMS = 0,
                          U_CHUNKS = 0, C_CHUNKS = 0, AD = 0, ZD = 1, RPTA = RPT;
     static_assert(TYO % RPT == 0 && C_ITEMS % 32 == 0, "full consumer warps");
+    template <int KB> static constexpr int DEPTH_K = DEPTH;
     static size_t smem_bytes() { return sizeof(double) * size_t(DEPTH) * Y_ELEMS; }
 };
 using CoarseP0 = CoarseCfgP<16, 8, 2, 2, 2>;   // default
@@ -778,7 +781,8 @@ template <int KB, class C>
 __global__ void __maxnreg__(C::MAXR)
 fused_persist_kernel(const StencilArgs a, const __grid_constant__ TmaMaps tm) {
     extern __shared__ __align__(128) double sm[];
-    __shared__ __align__(8) uint64_t full[C::ZD], empty[C::ZD], in_full[C::DEPTH], in_empty[C::DEPTH];
+    constexpr int DEPTH = C::template DEPTH_K<KB>;
+    __shared__ __align__(8) uint64_t full[C::ZD], empty[C::ZD], in_full[DEPTH], in_empty[DEPTH];
     const int items = a.tiles_x * a.tiles_y * a.chunks_z;
     if constexpr (C::FILL == 2) {
         if (smem_u32(sm) & 127) __trap();  // TMA destinations need 128-byte alignment
@@ -788,7 +792,7 @@ fused_persist_kernel(const StencilArgs a, const __grid_constant__ TmaMaps tm) {
             mbar_init(&full[s], C::NTA);
             mbar_init(&empty[s], C::NTB);
         }
-        for (int s = 0; s < C::DEPTH; ++s) {
+        for (int s = 0; s < DEPTH; ++s) {
             mbar_init(&in_full[s], C::NTP);
             mbar_init(&in_empty[s], C::template IN_CONSUMERS<KB>);
         }
