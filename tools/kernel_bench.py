@@ -2,7 +2,8 @@
 
     python tools/kernel_bench.py [n] [variants...]
 Prints per-step device times (CUDA events, warm, L2 flushed implicitly by
-fields > L2 at 256^3) and algorithmic GB/s; checks variants agree bitwise."""
+fields > L2 at 256^3; median of BENCH_REPS repetitions, default 5) and
+algorithmic GB/s; checks variants agree bitwise."""
 import os
 import sys
 
@@ -13,6 +14,7 @@ import paper_1409_8563_b200 as pr  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 variants = [v for v in sys.argv[2:]] or ["0", "1", "2", "3"]
 chunks = os.environ.get("BENCH_CHUNKS", "").split(",") if os.environ.get("BENCH_CHUNKS") else [None]
+REPS = int(os.environ.get("BENCH_REPS", "5"))
 ref = None
 u0 = None
 for ch in chunks:
@@ -47,18 +49,21 @@ for ch in chunks:
         pr.pr_fine(g, u0, u, 0, 32, dt)
         pr.pr_coarse(g, u0, u, 0, 64, Dt)
         torch.cuda.synchronize()
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         NF, NC = 64, 256
-        e[0].record()
-        pr.pr_fine(g, u0, u, 0, NF, dt)
-        e[1].record()
         w = torch.empty_like(u0)
-        e[2].record()
-        pr.pr_coarse(g, u0, w, 0, NC, Dt)
-        e[3].record()
-        torch.cuda.synchronize()
-        tf = e[0].elapsed_time(e[1]) / NF
-        tc = e[2].elapsed_time(e[3]) / NC
+        tfs, tcs = [], []
+        for _ in range(REPS):  # median of REPS timings (run-to-run spread is a few %)
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e[0].record()
+            pr.pr_fine(g, u0, u, 0, NF, dt)
+            e[1].record()
+            e[2].record()
+            pr.pr_coarse(g, u0, w, 0, NC, Dt)
+            e[3].record()
+            torch.cuda.synchronize()
+            tfs.append(e[0].elapsed_time(e[1]) / NF)
+            tcs.append(e[2].elapsed_time(e[3]) / NC)
+        tf, tc = sorted(tfs)[REPS // 2], sorted(tcs)[REPS // 2]
         same = None
         if ref is None:
             ref = (u.clone(), w.clone())
