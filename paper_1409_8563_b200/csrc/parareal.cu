@@ -138,6 +138,11 @@ struct pr_grid {
     // spatially coarsened G (NEXT-4): a child grid on the n/2 mesh and one field there
     pr_grid *half = nullptr;
     double *half_u = nullptr;
+    // concurrent F over a slice group (NEXT-2, small n): one child grid (own RK4 scratch,
+    // nu table, graphs) and one stream per slice; fork / join events
+    std::vector<pr_grid *> slice_grids;
+    std::vector<cudaStream_t> slice_streams;
+    std::vector<cudaEvent_t> slice_events;  // [0] fork, [1 + l] join of slice l
 };
 
 // cuStreamWaitValue32 through the runtime's driver entry point: the stream's
@@ -898,7 +903,10 @@ pr_status pr_destroy_grid(pr_grid *g) {
     cudaFree(g->d_flags); cudaFree(g->d_ipc);
     if (g->half) pr_destroy_grid(g->half);
     cudaFree(g->half_u);
+    for (pr_grid *c : g->slice_grids) pr_destroy_grid(c);
     cudaSetDevice(g->dev);
+    for (cudaStream_t t : g->slice_streams) cudaStreamDestroy(t);
+    for (cudaEvent_t e : g->slice_events) cudaEventDestroy(e);
     if (g->comm) ncclCommDestroy(g->comm);
     for (double *p : g->pool) cudaFree(p);
     cudaFree(g->acc); cudaFree(g->ya); cudaFree(g->yb); cudaFree(g->ctmp);
@@ -1281,6 +1289,35 @@ static pr_status post(pr_grid *g, double *stop_dst, double stop, unsigned int *f
     return PR_OK;
 }
 
+// Concurrent F over the s slices of a group: F of different slices of one iteration are
+// independent (each starts from the previous iteration's value), so for small n, where one
+// F launch does not fill the GPU, each slice runs on its own stream with its own child grid.
+static bool conc_wanted(const pr_grid *g, int s) {
+    const char *e = getenv("PR_CONC");
+    if (e) return s > 1 && e[0] == '1';
+    return s > 1 && g->n <= 64;
+}
+
+static pr_status ensure_slice_grids(pr_grid *g, int s) {
+    while (int(g->slice_grids.size()) < s) {
+        pr_grid *c = nullptr;
+        CKS(pr_create_grid(&g->prob, g->dev, &c));
+        g->slice_grids.push_back(c);
+    }
+    CK(cudaSetDevice(g->dev));
+    while (int(g->slice_streams.size()) < s) {
+        cudaStream_t t;
+        CK(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+        g->slice_streams.push_back(t);
+    }
+    while (int(g->slice_events.size()) < s + 1) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        g->slice_events.push_back(e);
+    }
+    return PR_OK;
+}
+
 pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, double *u_T,
                       const double *u_ref, double *defects_host, void *stream) {
     CKS(check_grid(g));
@@ -1395,6 +1432,8 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
     auto Fp = [&](const double *in, double *o, int m) -> pr_status {
         return run_fine(g, in, o, int64_t(m) * nf, nf, dt, st);
     };
+    const bool conc = conc_wanted(g, s);
+    if (conc) CKS(ensure_slice_grids(g, s));
     const size_t msg = size_t(g->N) + (ctrl ? 1 : 0);  // hand-off length (doubles)
 
     // peer mode: this rank's receive buffers are idle until its first receive
@@ -1430,9 +1469,19 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
             if (want_def) CKS(launch_maxabs(g, gold[s - 1], refd, g->d_red + 0, nullptr, st));
             break;
         case PR_OP_F:
-            CKS(Fp(start[l], f[l], op.slice));
+            if (conc) {  // fork at the first slice, join after the last
+                if (l == 0) CK(cudaEventRecord(g->slice_events[0], st));
+                cudaStream_t fs = g->slice_streams[l];
+                CK(cudaStreamWaitEvent(fs, g->slice_events[0], 0));
+                CKS(run_fine(g->slice_grids[l], start[l], f[l], int64_t(op.slice) * nf, nf, dt, fs));
+                CK(cudaEventRecord(g->slice_events[1 + l], fs));
+                if (l == s - 1)
+                    for (int ll = 0; ll < s; ++ll) CK(cudaStreamWaitEvent(st, g->slice_events[1 + ll], 0));
+            } else {
+                CKS(Fp(start[l], f[l], op.slice));
+            }
             // peer mode: start[0] (next iteration's receive buffer of the same parity) is free
-            if (peer && r > 0 && l == 0)
+            if (peer && r > 0 && (conc ? l == s - 1 : l == 0))
                 CKS(post(g, nullptr, 0.0, g->pred_flags + 1, base + unsigned(op.k) + 1, st));
             if (l == s - 1) {
                 CK(cudaEventRecord(evF(op.k), st));

@@ -374,3 +374,21 @@ def test_coarse_kernels_bitwise(n, variant, monkeypatch):
         outs.append(out)
         g.destroy()
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("n,Np,K", [(32, 4, 2), (64, 8, 3)])
+def test_concurrent_slices_bitwise(n, Np, K, monkeypatch):
+    """F over the slices of a group on concurrent streams (PR_CONC=1, one child grid per
+    slice) gives the sequential run's bits, defects included (NEXT-2)."""
+    u0 = dev(random_field(n, 53))
+    res = []
+    for conc in ("0", "1"):
+        monkeypatch.setenv("PR_CONC", conc)
+        g = pr.Grid(pr.Problem(n, c=PARITY_C, T=0.004))
+        uf = torch.empty_like(u0)
+        pr.pr_fine(g, u0, uf, 0, Np * 16, 0.004 / (Np * 16))
+        uT = torch.empty_like(u0)
+        d = pr.pr_parareal(g, pr.PararealCfg(Np, 4, 16, K), u0, uT, uf)
+        res.append((uT, d))
+        g.destroy()
+    assert torch.equal(res[0][0], res[1][0]) and res[0][1] == res[1][1]
