@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libparareal.so")
+# PR_LIB: an alternative build of the same library (e.g. the PRK_DEBUG index-checking build)
+LIB_PATH = os.environ.get("PR_LIB") or os.path.join(HERE, "libparareal.so")
 
 PR_OK, PR_EINVAL, PR_ENOMEM, PR_ECUDA, PR_ENCCL, PR_EDOMAIN, PR_ESTATE = range(7)
 STATUS_NAMES = {0: "PR_OK", 1: "PR_EINVAL", 2: "PR_ENOMEM", 3: "PR_ECUDA", 4: "PR_ENCCL",

@@ -12,6 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libparareal.so")
+LIB_DEBUG = os.path.join(HERE, "libparareal_debug.so")  # PRK_DEBUG: in-kernel index checks
 SRCS = [os.path.join(HERE, "csrc", "parareal.cu")]
 DEPS = SRCS + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "parareal.h")]
 
@@ -31,28 +32,30 @@ def nccl_dirs():
     return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
-def nvcc_cmd(out: str) -> list[str]:
+def nvcc_cmd(out: str, debug: bool = False) -> list[str]:
     inc, lib = nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     return [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
             "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared", "-Xptxas", "-v",
+            *(["-DPRK_DEBUG"] if debug else []),
             "-I", os.path.join(ROOT, "include"), "-I", inc,
             *SRCS, "-o", out, "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}"]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in DEPS):
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = nvcc_cmd(tmp)
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    lib = LIB_DEBUG if debug else LIB
+    if not force and os.path.exists(lib) and os.path.getmtime(lib) >= max(os.path.getmtime(d) for d in DEPS):
+        return lib
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = nvcc_cmd(tmp, debug)
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libparareal.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -239,6 +239,7 @@ __device__ __forceinline__ WorkItem decode_item(const StencilArgs &a, int item, 
     w.y0 = tiy * tyo;
     w.z_begin = b * a.cz;
     w.nz = min(a.cz, a.n - w.z_begin);
+    PRK_CHECK(w.x0 + txo <= a.n && w.y0 + tyo <= a.n && w.nz >= 1 && w.z_begin + w.nz <= a.n);
     return w;
 }
 
@@ -299,6 +300,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
                 line_order(c, C::IH, TXO / 2, C::HX / 2, r, cc);
                 ysrc[k] = wrap1(w.y0 - C::HY + r, n) * n + wrap1(w.x0 - C::HX + 2 * cc, n);
                 ydst[k] = 8 * (r * IW + 2 * cc);
+                PRK_CHECK(ysrc[k] >= 0 && ysrc[k] + 2 <= n * n && ydst[k] + 16 <= 8 * C::Y_ELEMS);
             }
         }
         int usrc[KB == K_B ? NU : 1], udst[KB == K_B ? NU : 1];
@@ -314,6 +316,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
                     line_order(c, C::EH, TXO / 2, 1, r, cc);
                     usrc[k] = wrap1(w.y0 - 2 + r, n) * n + wrap1(w.x0 - 2 + 2 * cc, n);
                     udst[k] = 8 * (r * EW + 2 * cc);
+                    PRK_CHECK(usrc[k] >= 0 && usrc[k] + 2 <= n * n && udst[k] + 16 <= 8 * C::Z_ELEMS);
                 }
             }
 #pragma unroll
@@ -325,6 +328,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
                     const int r = c / (TXO / 2), cc = c % (TXO / 2);
                     csrc[k] = (w.y0 + r) * n + w.x0 + 2 * cc;
                     cdst[k] = 8 * (C::Z_ELEMS + r * TXO + 2 * cc);
+                    PRK_CHECK(csrc[k] + 2 <= n * n && cdst[k] + 16 <= 8 * C::AUX_ELEMS);
                 }
             }
         }
@@ -414,6 +418,9 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
     const int r0 = g * RPT;
     const int sY = (r0 + 2) * IW + 2 * l + 2;
     const int sZ = r0 * EW + 2 * l;
+    // every shared access of this lane: x/y neighbours of its RPT rows, its Z-ring rows
+    PRK_CHECK(sY - 2 * IW - 2 >= 0 && sY + (RPT + 1) * IW + 4 <= C::Y_ELEMS);
+    PRK_CHECK(sZ >= 0 && sZ + (RPT - 1) * EW + 2 <= C::Z_ELEMS);
     const bool tcol = l >= 1 && l <= TXO / 2;
     const int tp0 = (r0 - 2) * TXO + 2 * l - 2;
 
@@ -492,6 +499,7 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                     const int er = r0 + r;
                     if (outp && tcol && er >= 2 && er < C::TYO + 2) {
                         const int tp = tp0 + r * TXO;
+                        PRK_CHECK(tp >= 0 && tp + 2 <= C::T_ELEMS);
                         if (KB == K_A) {
                             double2 t0;
                             t0.x = yc.x + (dt / 6.0) * k[r].x;
@@ -536,6 +544,8 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
     const int r0 = g * RPT;
     const int sZ = (r0 + 2) * EW + 2 * m + 2;
     const int sT = r0 * TXO + 2 * m;
+    PRK_CHECK(sZ - 2 * EW - 2 >= 0 && sZ + (RPT + 1) * EW + 4 <= C::Z_ELEMS);
+    PRK_CHECK(sT >= 0 && sT + (RPT - 1) * TXO + 2 <= C::T_ELEMS);
     const double *yring = sm;
     const int sU = (r0 + C::HY) * C::IWS + 2 * m + C::HX;  // tile point in an input slot
 
@@ -673,6 +683,7 @@ __device__ __forceinline__ void stage_c_p(const StencilArgs &a, double *sm, int 
     const int m = t % (TXO / 2), g = t / (TXO / 2);
     const int r0 = g * RPT;
     const int sY = (r0 + C::HY) * IW + 2 * m + C::HX;
+    PRK_CHECK(sY - IW - 2 >= 0 && sY + RPT * IW + 4 <= C::Y_ELEMS);
 
     // folded weights of Alg.2 (same expressions as stencil_kernel<K_COARSE>)
     const double nu = a.nu_tab[*a.nu_pos + a.j_local];

@@ -24,6 +24,20 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// PRK_DEBUG builds (paper_1409_8563_b200/build.py debug=True) check shared-memory and
+// global index ranges inside the kernels and trap on a violation (compute-sanitizer is not
+// available on the GPU pool); release builds compile the checks away.
+#ifdef PRK_DEBUG
+#define PRK_CHECK(cond)          \
+    do {                         \
+        if (!(cond)) __trap();   \
+    } while (0)
+#else
+#define PRK_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 namespace prk {
 
 enum Kind { K_COARSE = 0, K_S1 = 1, K_S2 = 2, K_S3 = 3, K_S4 = 4 };
