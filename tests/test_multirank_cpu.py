@@ -1,4 +1,4 @@
-"""World-size-2 (and 4) CPU test of the multi-rank host logic over torch.distributed
+"""World-size-2 (and 4, 8) CPU test of the multi-rank host logic over torch.distributed
 gloo: every rank executes the schedule the C library emits (pr_plan) with the
 oracle's F and G and real point-to-point send/recv; the last rank's u_T and
 defect history must equal the oracle's serial Alg.1 emulation bitwise (the
@@ -126,7 +126,8 @@ def worker(rank, W, port, Np, K, q, tol=0.0):
 
 
 @pytest.mark.parametrize("W,Np,K,tol", [(2, 2, 1, 0.0), (2, 2, 2, 0.0), (2, 4, 2, 0.0), (2, 4, 3, 0.0),
-                                        (4, 4, 2, 0.0), (2, 4, 4, 3e-3), (2, 4, 4, 1e-6), (4, 4, 4, 1e-6)])
+                                        (4, 4, 2, 0.0), (2, 4, 4, 3e-3), (2, 4, 4, 1e-6), (4, 4, 4, 1e-6),
+                                        (8, 8, 3, 0.0)])  # the bench's 8-GPU schedule
 def test_pipelined_plan_matches_serial_alg1(W, Np, K, tol, orc):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
