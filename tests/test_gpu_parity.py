@@ -270,6 +270,23 @@ def test_full_size_steps_vs_oracle(n):
     assert rel(out, oracle.coarse(p, u0, 500, 3, Dt)) <= TOL
 
 
+def test_cfg4_512_steps_vs_oracle():
+    """cfg4 (512^3, 1 GiB per field; T = 0.1/32, N_t = 2^14, N_C = 2^10) in the
+    launch configuration bench.py --config cfg4 times: one fine and one coarse step at a late
+    step index, every output point against the oracle (≈ 3 s of 16-thread oracle work)."""
+    n, T = 512, 0.1 / 32
+    u0 = random_field(n, 21)
+    g = pr.Grid(pr.Problem(n, c=(1.0, 1.0, 1.0), T=T))
+    p = oproblem(n, c=(1.0, 1.0, 1.0), T=T)
+    dt, Dt = T / 2 ** 14, T / 2 ** 10
+    out = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+    pr.pr_fine(g, dev(u0), out, 2 ** 14 - 1, 1, dt)
+    assert rel(out, oracle.fine(p, u0, 2 ** 14 - 1, 1, dt)) <= TOL
+    pr.pr_coarse(g, dev(u0), out, 2 ** 10 - 1, 1, Dt)
+    assert rel(out, oracle.coarse(p, u0, 2 ** 10 - 1, 1, Dt)) <= TOL
+    g.destroy()
+
+
 @pytest.mark.parametrize("f2", ["1", "0"])
 @pytest.mark.parametrize("n", [32, 64, 128])
 def test_run_twice_bitwise(n, f2, monkeypatch):
