@@ -53,7 +53,9 @@ typedef enum {
     PR_EINVAL = 1,   /* bad argument: null pointer, n odd or < 4, n_steps < 0, dt <= 0, ... */
     PR_ENOMEM = 2,   /* device or pinned-host allocation failed */
     PR_ECUDA = 3,    /* CUDA runtime error */
-    PR_ENCCL = 4,    /* NCCL error; message carries rank and iteration */
+    PR_ENCCL = 4,    /* hand-off failure (NCCL error, or a peer rank that did not deliver
+                        within PR_NCCL_TIMEOUT_S, default 900 s); message carries rank and
+                        iteration */
     PR_EDOMAIN = 5,  /* ||u_ref||_inf = 0 in a defect (Eq.(defect) undefined) */
     PR_ESTATE = 6    /* call not valid in this state (e.g. world > 1 before pr_comm_init) */
 } pr_status;
@@ -153,6 +155,24 @@ pr_status pr_correct(pr_grid *grid, const double *f, const double *g_new, const 
 pr_status pr_nccl_unique_id(void *id_out);
 pr_status pr_comm_init(pr_grid *grid, int32_t world, int32_t rank, const void *nccl_unique_id);
 
+/* In-process rank group: links `world` grids of THIS process (on one device or on
+ * several devices with peer access) as ranks 0..world-1 of one time-slice pipeline,
+ * without NCCL (replaces a communicator; pr_comm_init on a member leaves the group).
+ * Each grid is then driven by its own host thread calling pr_parareal with the same
+ * cfg; every rank's work runs on its grid's own stream (joined to the caller's stream
+ * by events).  Hand-off (Alg.1): the correction pass of rank r's last
+ * slice stores u^{k+1} straight into rank r+1's receive buffer (the peer-store data
+ * path of PR_FLAG_PEER_HANDOFF, here a plain device or peer pointer); rank r records a
+ * CUDA event after it and announces it through the group, and rank r+1's stream waits
+ * on that event before its G reads the buffer; rank r+1 releases the buffer the same
+ * way after the F that last reads it.  No stream or kernel waits on a value that has
+ * not been announced, so ranks may share one GPU.  A rank that hears nothing from its
+ * peer for PR_NCCL_TIMEOUT_S seconds (default 900) fails with PR_ENCCL (rank and
+ * iteration in the message).  Grids must outlive the group's calls.  Errors:
+ * PR_EINVAL (NULL or repeated grid, no peer access between consecutive devices),
+ * PR_ECUDA. */
+pr_status pr_local_group(pr_grid **grids, int32_t world);
+
 /* Alg.1 for this rank's slice group: rank r of W owns slices
  * [r s, (r+1) s), s = N_p / W (W = 1 without pr_comm_init).  u0: initial value
  * (every rank; host or device).  u_T: receives u^K_{N_p} on the LAST rank
@@ -177,6 +197,9 @@ pr_status pr_comm_init(pr_grid *grid, int32_t world, int32_t rank, const void *n
  * waits on that word (cuStreamWaitValue32: the stream front end waits, no
  * kernel spins); the successor hands its receive buffer back the same way
  * after the F that last reads it.  Results are bitwise those of the NCCL path.
+ * The consumer's stream wait uses CU_STREAM_WAIT_VALUE_FLUSH where the device supports
+ * it and is followed by a one-thread ld.acquire.sys + fence.acq_rel.sys kernel before
+ * G reads the buffer.
  * Errors: PR_EINVAL, PR_ESTATE (world > 1 without a communicator), PR_ENCCL,
  * PR_EDOMAIN (u_ref all zero), PR_ECUDA. */
 pr_status pr_parareal(pr_grid *grid, const pr_parareal_cfg *cfg, const double *u0,

@@ -24,7 +24,7 @@ __all__ = ["Problem", "PararealCfg", "Grid", "pr_create_grid", "pr_destroy_grid"
            "pr_comm_init", "pr_parareal", "pr_plan", "pr_last_timings", "pr_kernel_launches",
            "pr_stability_ratio", "pr_last_error", "pr_version", "pr_grid_info", "pr_last_monitors", "PrError", "PR_NU_STAGE",
            "PR_NU_STEP_START", "PR_FLAG_G_IS_F", "PR_FLAG_PEER_HANDOFF", "PR_FLAG_G_HALF_MESH",
-           "pr_coarse_mesh", "comm_init_torch"]
+           "pr_coarse_mesh", "comm_init_torch", "pr_local_group"]
 
 
 @dataclass
@@ -227,6 +227,13 @@ def pr_comm_init(grid, world: int, rank: int, unique_id: bytes) -> None:
         raise ValueError("unique id must be 128 bytes")
     buf = ctypes.create_string_buffer(unique_id, PR_NCCL_ID_BYTES)
     _lib.check(_lib.load().pr_comm_init(grid.handle, int(world), int(rank), buf))
+
+
+def pr_local_group(grids) -> None:
+    """Link grids of this process as ranks 0..W-1 of one pipeline (no NCCL); each is
+    then driven by its own thread calling pr_parareal (ctypes releases the GIL)."""
+    arr = (ctypes.c_void_p * len(grids))(*[g.handle.value for g in grids])
+    _lib.check(_lib.load().pr_local_group(arr, len(grids)))
 
 
 def comm_init_torch(grid) -> None:

@@ -28,7 +28,7 @@ OPS = {1: "G_PREFIX", 2: "G_INIT", 3: "DEFECT0", 4: "F", 5: "RECV", 6: "G", 7: "
 EXPORTS = ["pr_create_grid", "pr_destroy_grid", "pr_fine", "pr_coarse", "pr_coarse_mesh", "pr_defect",
            "pr_fill_sine", "pr_correct", "pr_nccl_unique_id", "pr_comm_init", "pr_parareal",
            "pr_plan", "pr_last_timings", "pr_kernel_launches", "pr_stability_ratio",
-           "pr_last_error", "pr_version", "pr_grid_info", "pr_last_monitors"]
+           "pr_last_error", "pr_version", "pr_grid_info", "pr_last_monitors", "pr_local_group"]
 
 
 class PrProblem(ctypes.Structure):
@@ -92,6 +92,7 @@ def load() -> ctypes.CDLL:
         "pr_version": (ctypes.c_char_p, []),
         "pr_grid_info": (st, [vp, ctypes.POINTER(PrGridInfo)]),
         "pr_last_monitors": (st, [vp, ctypes.POINTER(dbl), i32, ctypes.POINTER(i32)]),
+        "pr_local_group": (st, [ctypes.POINTER(vp), i32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

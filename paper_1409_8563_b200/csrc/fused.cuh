@@ -169,6 +169,7 @@ __device__ __forceinline__ double2 apply_pair(const Weights &W, double2 L, doubl
 template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_, int PW_ = 1, int FILL_ = 0,
           int UIN_ = 0, int DEPTHA_ = DEPTH_>
 struct FusedCfgP {
+    static constexpr bool COMB = false;  // comb.cuh configs: stage B in the stage-A lanes
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = 1, XP = 2,
                          PROD = 1, PW = PW_;  // PW producer warps
     // FILL 0: every plane by 16-byte cp.async; 2: planes of tiles away from the
@@ -211,16 +212,22 @@ struct FusedCfgP {
                                  size_t(ZD) * ZS_ELEMS<KB>);
     }
 };
+using FusedP4 = FusedCfgP<16, 9, 4, 2, 2, 2, 2>;  // 32x16 tile, TMA tensor fills (default, PR_FTILE=14)
+// 32x32 output tile, four rows per lane in both stages (12 warps): stage A's halo ring
+// recomputes 27 % instead of 41 %, and each lane reads 2 instead of 2.5 shared values per point
+using FusedT32 = FusedCfgP<32, 7, 4, 4, 4, 2, 2, 0, 7>;
+using FusedT32B = FusedCfgP<32, 5, 3, 4, 4, 2, 2, 0, 5>;  // K_B at 32x32: shallower rings to fit
+#ifdef PRK_VARIANTS  // tuning history (profiles/r01_kernel_bench_variants.txt)
 using FusedP0 = FusedCfgP<16, 7, 4, 2, 2, 1>;   // one producer warp
 using FusedP1 = FusedCfgP<16, 9, 4, 2, 2, 1>;
 using FusedP2 = FusedCfgP<16, 8, 5, 2, 2, 2>;   // 5-slot intermediate ring
 using FusedP3 = FusedCfgP<16, 9, 4, 2, 2, 2>;     // two producer warps, cp.async only
-using FusedP4 = FusedCfgP<16, 9, 4, 2, 2, 2, 2>;  // + TMA tensor fills (default, PR_FTILE=14)
 using FusedP5 = FusedCfgP<16, 9, 5, 2, 2, 2, 2>;  // + 5-slot intermediate ring
 using FusedP6 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 1>;  // + K_A stage B reads u from the input ring
 using FusedP7 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 12>;  // 12-slot input ring in K_A
 using FusedP8 = FusedCfgP<16, 9, 4, 4, 4, 2, 2>;  // four rows per lane (7 warps: <= 256 threads at ~190 regs)
 using FusedP9 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 1, 13>;  // UIN + 13-slot input ring in K_A
+#endif
 
 struct WorkItem {
     int x0, y0, z_begin, nz;
@@ -656,8 +663,10 @@ struct CoarseCfgP {
     static size_t smem_bytes() { return sizeof(double) * size_t(DEPTH) * Y_ELEMS; }
 };
 using CoarseP0 = CoarseCfgP<16, 8, 2, 2, 2>;   // default
+#ifdef PRK_VARIANTS
 using CoarseP1 = CoarseCfgP<16, 8, 1, 2, 2>;   // one row per lane (8 consumer warps)
 using CoarseP2 = CoarseCfgP<16, 10, 2, 1, 2>;
+#endif
 
 template <class Body>
 __device__ __forceinline__ void rotating_loop3(int NJ, Body &&body) {

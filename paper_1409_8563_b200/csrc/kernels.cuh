@@ -53,10 +53,12 @@ template <int TY_, int RPT_, int DEPTH_> struct TileCfg {
     static constexpr int NTHREADS = TX * BY;
     static_assert(TY % RPT == 0, "TY must be a multiple of RPT");
 };
-using Tile0 = TileCfg<16, 4, 7>;   // 128 threads
+using Tile0 = TileCfg<16, 4, 7>;   // 128 threads (default)
+#ifdef PRK_VARIANTS
 using Tile1 = TileCfg<16, 2, 7>;   // 256 threads
 using Tile2 = TileCfg<32, 4, 6>;   // 256 threads, larger tile (less halo re-read)
 using Tile3 = TileCfg<8, 2, 8>;    // 128 threads, small slots (3-4 CTAs/SM)
+#endif
 
 template <int KIND> struct Traits;
 template <> struct Traits<K_COARSE> { static constexpr int R = 1, NP = 0; };
@@ -475,6 +477,15 @@ __global__ void post_kernel(double *stop_dst, double stop, unsigned int *flag, u
     if (stop_dst) *stop_dst = stop;
     __threadfence_system();
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(seq) : "memory");
+}
+
+// Consumer side of a peer hand-off, after the stream has waited for the sequence word:
+// an acquire load of the word at system scope plus a system fence, so that every later
+// kernel of this stream observes the data stores that preceded the producer's release.
+// One thread; the value is already published when this runs (no spinning).
+__global__ void acquire_kernel(const unsigned int *flag) {
+    asm volatile("{\n\t.reg .u32 t;\n\tld.acquire.sys.global.u32 t, [%0];\n\t}" ::"l"(flag) : "memory");
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
 // *d_diff = max|u - ref| (if u and d_diff), *d_ref = max|ref| (if d_ref)

@@ -15,7 +15,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <utility>
@@ -24,6 +27,7 @@
 #include "../../include/parareal.h"
 #include "kernels.cuh"
 #include "fused.cuh"
+#include "comb.cuh"
 
 using namespace prk;
 
@@ -81,6 +85,33 @@ struct NuTable {
 constexpr int FINE_BATCH = 16;    // RK4 steps per CUDA graph (64 kernels)
 constexpr int COARSE_PAIRS = 16;  // Euler step pairs per CUDA graph (32 kernels)
 
+// In-process rank group (pr_local_group): W grids of one process (on one device or
+// several) linked as ranks 0..W-1 of the time-slice pipeline without NCCL.  The
+// hand-off data path is the peer path's (the correction kernel stores u^{k+1} into the
+// successor's receive buffer); ordering goes through CUDA events whose records the
+// ranks' host threads announce to each other here, so no stream or kernel ever waits
+// on a value another rank has not yet been told to produce.
+struct LocalRank {
+    unsigned long long started = 0;  // base + 1 of the call in progress (0: none yet)
+    unsigned long long data = 0;     // last hand-off published: base + k + 1
+    unsigned long long freed = 0;    // last receive-buffer release published: base + k + 1
+    double *mail[2] = {nullptr, nullptr};  // this rank's two receive buffers (k even / odd)
+    std::vector<cudaEvent_t> ev_data, ev_free;  // recorded on the rank's stream per iteration
+    int dev = 0;
+};
+struct LocalGroup {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<LocalRank> r;
+    ~LocalGroup() {
+        for (LocalRank &x : r) {
+            cudaSetDevice(x.dev);
+            for (cudaEvent_t e : x.ev_data) cudaEventDestroy(e);
+            for (cudaEvent_t e : x.ev_free) cudaEventDestroy(e);
+        }
+    }
+};
+
 }  // namespace
 
 struct pr_grid {
@@ -109,7 +140,14 @@ struct pr_grid {
     size_t h_stage_cap = 0;
     cudaEvent_t stage_ev = nullptr;         // last table upload
     LaunchCfg lc[5];
-    std::map<std::pair<int, const void *>, std::pair<cudaGraphExec_t, int>> graphs;
+    // cached CUDA graphs keyed by (kind, state buffer); each remembers the exact step
+    // size and nu-table pointer it was captured with
+    struct CachedGraph {
+        cudaGraphExec_t exec;
+        double dt;
+        const double *tab;
+    };
+    std::map<std::pair<int, const void *>, CachedGraph> graphs;
     // host-pointer staging
     double *stage_a = nullptr, *stage_b = nullptr;
     // Parareal state
@@ -143,6 +181,14 @@ struct pr_grid {
     std::vector<pr_grid *> slice_grids;
     std::vector<cudaStream_t> slice_streams;
     std::vector<cudaEvent_t> slice_events;  // [0] fork, [1 + l] join of slice l
+    // in-process rank group (pr_local_group): shared state, this grid's rank, and the
+    // grid's own compute stream (the caller's stream is joined by events)
+    std::shared_ptr<LocalGroup> lgroup;
+    cudaStream_t work_stream = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    // peer hand-off ordering on the consumer side: CU_STREAM_WAIT_VALUE_FLUSH if the
+    // device can flush remote writes (-1: not queried yet)
+    int can_flush = -1;
 };
 
 // cuStreamWaitValue32 through the runtime's driver entry point: the stream's
@@ -186,60 +232,6 @@ static bool tma_encode3(CUtensorMap *m, const double *p, int n, int bx, int by) 
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int KIND, class C>
-static pr_status setup_kind_cfg(pr_grid *g) {
-    const size_t smem = Layout<KIND, C>::SMEM_BYTES;
-    CK(cudaFuncSetAttribute(stencil_kernel<KIND, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(smem)));
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil_kernel<KIND, C>, C::NTHREADS,
-                                                     smem));
-    if (occ < 1) return fail(PR_ECUDA, "stencil kernel %d cannot be resident", KIND);
-    LaunchCfg &c = g->lc[KIND];
-    const int n = g->n;
-    c.occ = occ;
-    c.threads = C::NTHREADS;
-    c.smem = smem;
-    c.tiles_x = (n + TX - 1) / TX;
-    c.tiles_y = (n + C::TY - 1) / C::TY;
-    const int tiles = c.tiles_x * c.tiles_y;
-    const int slots = g->sms * occ;
-    const int R = Traits<KIND>::R;
-    // z-chunking: fill whole waves of resident CTAs while keeping the z halo
-    // re-read (2R planes per chunk) small.
-    int best_chunks = 1;
-    double best = -1.0;
-    const int min_cz = std::min(n, 8);
-    for (int ch = 1; ch <= n / min_cz; ++ch) {
-        const int cz = (n + ch - 1) / ch;
-        const int che = (n + cz - 1) / cz;
-        const long items = long(tiles) * che;
-        const long waves = (items + slots - 1) / slots;
-        const double eff = double(items) / double(waves * slots);
-        const double over = 1.0 + 0.5 * double(2 * R) / double(cz);
-        const double score = eff / over;
-        if (score > best + 1e-9) { best = score; best_chunks = che; }
-    }
-    if (const char *env = getenv("PR_CHUNKS_Z")) {
-        int v = atoi(env);
-        if (v >= 1 && v <= n) best_chunks = v;
-    }
-    c.cz = (n + best_chunks - 1) / best_chunks;
-    c.chunks_z = (n + c.cz - 1) / c.cz;
-    c.blocks = tiles * c.chunks_z;
-    return PR_OK;
-}
-
-template <int KIND>
-static pr_status setup_kind(pr_grid *g) {
-    switch (g->variant) {
-    case 1: return setup_kind_cfg<KIND, Tile1>(g);
-    case 2: return setup_kind_cfg<KIND, Tile2>(g);
-    case 3: return setup_kind_cfg<KIND, Tile3>(g);
-    default: return setup_kind_cfg<KIND, Tile0>(g);
-    }
-}
-
 // z-chunk count that fills whole waves of resident CTAs with little halo re-read
 static int pick_chunks(int n, int tiles, int slots, int halo) {
     int best_chunks = 1;
@@ -262,16 +254,62 @@ static int pick_chunks(int n, int tiles, int slots, int halo) {
     return best_chunks;
 }
 
+template <int KIND, class C>
+static pr_status setup_kind_cfg(pr_grid *g) {
+    const size_t smem = Layout<KIND, C>::SMEM_BYTES;
+    CK(cudaFuncSetAttribute(stencil_kernel<KIND, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(smem)));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil_kernel<KIND, C>, C::NTHREADS,
+                                                     smem));
+    if (occ < 1) return fail(PR_ECUDA, "stencil kernel %d cannot be resident", KIND);
+    LaunchCfg &c = g->lc[KIND];
+    const int n = g->n;
+    c.occ = occ;
+    c.threads = C::NTHREADS;
+    c.smem = smem;
+    c.tiles_x = (n + TX - 1) / TX;
+    c.tiles_y = (n + C::TY - 1) / C::TY;
+    const int tiles = c.tiles_x * c.tiles_y;
+    const int slots = g->sms * occ;
+    const int best_chunks = pick_chunks(n, tiles, slots, Traits<KIND>::R);
+    c.cz = (n + best_chunks - 1) / best_chunks;
+    c.chunks_z = (n + c.cz - 1) / c.cz;
+    c.blocks = tiles * c.chunks_z;
+    return PR_OK;
+}
+
+template <int KIND>
+static pr_status setup_kind(pr_grid *g) {
+    switch (g->variant) {
+#ifdef PRK_VARIANTS
+    case 1: return setup_kind_cfg<KIND, Tile1>(g);
+    case 2: return setup_kind_cfg<KIND, Tile2>(g);
+    case 3: return setup_kind_cfg<KIND, Tile3>(g);
+#endif
+    case 0: return setup_kind_cfg<KIND, Tile0>(g);
+    default: return fail(PR_EINVAL, "four-stage tile variant %d is not built (PRK_VARIANTS)", g->variant);
+    }
+}
+
+// the kernel of a fused-F config: separate stage-B warps (fused.cuh) or stage B in the
+// stage-A lanes (comb.cuh)
+template <int KB, class C>
+static constexpr auto fused_kernel_of() {
+    if constexpr (C::COMB) return &fused_comb_kernel<KB, C>;
+    else return &fused_persist_kernel<KB, C>;
+}
+
 template <int KB, class C>
 static pr_status setup_fused_persist(pr_grid *g) {
     const size_t smem = C::template smem_bytes<KB>();
-    CK(cudaFuncSetAttribute(fused_persist_kernel<KB, C>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    constexpr auto kern = fused_kernel_of<KB, C>();
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_persist_kernel<KB, C>, C::NT, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT, smem));
     if (occ < 1) {
         cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, fused_persist_kernel<KB, C>);
+        cudaFuncGetAttributes(&fa, kern);
         return fail(PR_ECUDA,
                     "persistent fused kernel %d cannot be resident (%d threads, %d regs, %zu B smem, "
                     "max threads %d)",
@@ -318,9 +356,12 @@ static pr_status setup_coarse_persist(pr_grid *g) {
 
 static pr_status setup_coarse(pr_grid *g) {
     switch (g->cvariant) {
+#ifdef PRK_VARIANTS
     case 1: return setup_coarse_persist<CoarseP1>(g);
     case 2: return setup_coarse_persist<CoarseP2>(g);
-    default: return setup_coarse_persist<CoarseP0>(g);
+#endif
+    case 0: return setup_coarse_persist<CoarseP0>(g);
+    default: return fail(PR_EINVAL, "coarse variant %d is not built (PRK_VARIANTS)", g->cvariant);
     }
 }
 
@@ -344,20 +385,39 @@ static void launch_coarse_persist(pr_grid *g, const StencilArgs &a0, cudaStream_
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
+// Fused F variants (PR_FTILE): the tile configuration of each of the two kernels
+// (K_A: stages 1+2, K_B: stages 3+4; they are independent launches over the whole
+// grid, so their tilings may differ).  X(id, config of K_A, config of K_B)
+#define PRK_FVARIANTS(X) \
+    X(14, FusedP4, FusedP4) X(20, FusedT32, FusedP4) X(21, FusedT32, FusedT32B) X(22, Comb16, Comb16)
+#ifdef PRK_VARIANTS
+#define PRK_FVARIANTS_OLD(X)                                                                    \
+    X(10, FusedP0, FusedP0) X(11, FusedP1, FusedP1) X(12, FusedP2, FusedP2) X(13, FusedP3, FusedP3) \
+    X(15, FusedP5, FusedP5) X(16, FusedP6, FusedP6) X(17, FusedP7, FusedP7) X(18, FusedP8, FusedP8) \
+    X(19, FusedP9, FusedP9)
+#else
+#define PRK_FVARIANTS_OLD(X)
+#endif
+template <int KB, class CA, class CB> using PickCfg = std::conditional_t<KB == K_A, CA, CB>;
+
+// output tile heights of a fused variant's two kernels (0, 0: not built)
+static void fused_tiles(int v, int *tya, int *tyb) {
+    *tya = *tyb = 0;
+    switch (v) {
+#define X(id, A, B) case id: *tya = A::TYO; *tyb = B::TYO; break;
+        PRK_FVARIANTS(X) PRK_FVARIANTS_OLD(X)
+#undef X
+    default: break;
+    }
+}
+
 template <int KB>
 static pr_status setup_fused(pr_grid *g) {
     switch (g->fvariant) {
-    case 10: return setup_fused_persist<KB, FusedP0>(g);
-    case 11: return setup_fused_persist<KB, FusedP1>(g);
-    case 12: return setup_fused_persist<KB, FusedP2>(g);
-    case 13: return setup_fused_persist<KB, FusedP3>(g);
-    case 14: return setup_fused_persist<KB, FusedP4>(g);
-    case 15: return setup_fused_persist<KB, FusedP5>(g);
-    case 16: return setup_fused_persist<KB, FusedP6>(g);
-    case 17: return setup_fused_persist<KB, FusedP7>(g);
-    case 18: return setup_fused_persist<KB, FusedP8>(g);
-    case 19: return setup_fused_persist<KB, FusedP9>(g);
-    default: return setup_fused_persist<KB, FusedP4>(g);
+#define X(id, A, B) case id: return setup_fused_persist<KB, PickCfg<KB, A, B>>(g);
+        PRK_FVARIANTS(X) PRK_FVARIANTS_OLD(X)
+#undef X
+    default: return fail(PR_EINVAL, "fused variant %d is not built (PRK_VARIANTS)", g->fvariant);
     }
 }
 
@@ -376,7 +436,8 @@ static void launch_persist(pr_grid *g, const StencilArgs &a, const LaunchCfg &c,
             return;
         }
     }
-    fused_persist_kernel<KB, C><<<c.blocks, c.threads, c.smem, st>>>(a, tm);
+    constexpr auto kern = fused_kernel_of<KB, C>();
+    kern<<<c.blocks, c.threads, c.smem, st>>>(a, tm);
 }
 
 template <int KB>
@@ -388,17 +449,10 @@ static void launch_fused(pr_grid *g, const StencilArgs &a0, cudaStream_t st) {
     a.cz = c.cz;
     a.chunks_z = c.chunks_z;
     switch (g->fvariant) {
-    case 10: launch_persist<KB, FusedP0>(g, a, c, st); break;
-    case 11: launch_persist<KB, FusedP1>(g, a, c, st); break;
-    case 12: launch_persist<KB, FusedP2>(g, a, c, st); break;
-    case 13: launch_persist<KB, FusedP3>(g, a, c, st); break;
-    case 14: launch_persist<KB, FusedP4>(g, a, c, st); break;
-    case 15: launch_persist<KB, FusedP5>(g, a, c, st); break;
-    case 16: launch_persist<KB, FusedP6>(g, a, c, st); break;
-    case 17: launch_persist<KB, FusedP7>(g, a, c, st); break;
-    case 18: launch_persist<KB, FusedP8>(g, a, c, st); break;
-    case 19: launch_persist<KB, FusedP9>(g, a, c, st); break;
-    default: launch_persist<KB, FusedP4>(g, a, c, st); break;
+#define X(id, A, B) case id: launch_persist<KB, PickCfg<KB, A, B>>(g, a, c, st); break;
+        PRK_FVARIANTS(X) PRK_FVARIANTS_OLD(X)
+#undef X
+    default: break;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -425,9 +479,11 @@ static void launch_stencil(pr_grid *g, const StencilArgs &a0, cudaStream_t st) {
     a.cz = c.cz;
     a.chunks_z = c.chunks_z;
     switch (g->variant) {
+#ifdef PRK_VARIANTS
     case 1: stencil_kernel<KIND, Tile1><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     case 2: stencil_kernel<KIND, Tile2><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     case 3: stencil_kernel<KIND, Tile3><<<c.blocks, c.threads, c.smem, st>>>(a); break;
+#endif
     default: stencil_kernel<KIND, Tile0><<<c.blocks, c.threads, c.smem, st>>>(a); break;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -484,8 +540,10 @@ static void enqueue_coarse_step(pr_grid *g, const double *src, double *dst, int 
     a.o0 = dst;
     if (g->c2) {
         switch (g->cvariant) {
+#ifdef PRK_VARIANTS
         case 1: launch_coarse_persist<CoarseP1>(g, a, st); break;
         case 2: launch_coarse_persist<CoarseP2>(g, a, st); break;
+#endif
         default: launch_coarse_persist<CoarseP0>(g, a, st); break;
         }
     } else {
@@ -507,8 +565,8 @@ static inline double nu_of(const pr_problem &p, double t) {
 
 static void clear_graphs(pr_grid *g, int kind) {
     for (auto it = g->graphs.begin(); it != g->graphs.end();) {
-        if (it->first.first == kind) {
-            cudaGraphExecDestroy(it->second.first);
+        if (kind < 0 || it->first.first == kind) {
+            cudaGraphExecDestroy(it->second.exec);
             it = g->graphs.erase(it);
         } else {
             ++it;
@@ -530,7 +588,12 @@ static pr_status ensure_table(pr_grid *g, int fine, double dt, int64_t lo, int64
         const size_t cap = std::max(need, T.cap * 2);
         CK(cudaMalloc(&T.d, cap * sizeof(double)));
         T.cap = cap;
-        clear_graphs(g, fine ? 0 : 1);  // graphs captured the old table pointer
+        if (fine) {  // graphs captured the old table pointer (four-pass and fused)
+            clear_graphs(g, 0);
+            clear_graphs(g, 2);
+        } else {
+            clear_graphs(g, 1);
+        }
     }
     if (need > g->h_stage_cap) {
         CK(cudaEventSynchronize(g->stage_ev));
@@ -569,13 +632,14 @@ static pr_status ensure_table(pr_grid *g, int fine, double dt, int64_t lo, int64
 // through the table (re-captured when the table pointer changes).
 static pr_status get_graph(pr_grid *g, int kind, double *u, double dt, cudaGraphExec_t *out) {
     auto key = std::make_pair(kind, (const void *)u);
+    const double *tab = kind == 1 ? g->tab_c.d : g->tab_f.d;
     auto it = g->graphs.find(key);
-    if (it != g->graphs.end() && it->second.second == int(std::hash<double>{}(dt) & 0x7fffffff)) {
-        *out = it->second.first;
+    if (it != g->graphs.end() && it->second.dt == dt && it->second.tab == tab) {
+        *out = it->second.exec;
         return PR_OK;
     }
     if (it != g->graphs.end()) {
-        cudaGraphExecDestroy(it->second.first);
+        cudaGraphExecDestroy(it->second.exec);
         g->graphs.erase(it);
     }
     cudaGraph_t graph;
@@ -606,11 +670,8 @@ static pr_status get_graph(pr_grid *g, int kind, double *u, double dt, cudaGraph
     cudaGraphDestroy(graph);
     if (ce != cudaSuccess)
         return fail(PR_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
-    if (g->graphs.size() > 64) {  // bound the cache
-        clear_graphs(g, 0);
-        clear_graphs(g, 1);
-    }
-    g->graphs[key] = std::make_pair(exec, int(std::hash<double>{}(dt) & 0x7fffffff));
+    if (g->graphs.size() > 64) clear_graphs(g, -1);  // bound the cache (every kind)
+    g->graphs[key] = pr_grid::CachedGraph{exec, dt, tab};
     *out = exec;
     return PR_OK;
 }
@@ -836,7 +897,7 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
     g->N = int64_t(n) * n * n;
     g->bytes = size_t(g->N) * sizeof(double);
     g->sms = prop.multiProcessorCount;
-    if (const char *tv = getenv("PR_TILE")) g->variant = std::max(0, std::min(3, atoi(tv)));
+    if (const char *tv = getenv("PR_TILE")) g->variant = atoi(tv);
     auto bail = [&](pr_status s) { pr_destroy_grid(g); return s; };
 #define GK(call)                                                                            \
     do {                                                                                    \
@@ -868,8 +929,11 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
     if ((s = setup_kind<K_S4>(g)) != PR_OK) return bail(s);
     {
         const char *fe = getenv("PR_F2");
-        if (const char *fv = getenv("PR_FTILE")) g->fvariant = std::max(10, std::min(19, atoi(fv)));
-        g->f2 = (n % FusedP4::TXO == 0) && (n % FusedP4::TYO == 0) && !(fe && fe[0] == '0');
+        if (const char *fv = getenv("PR_FTILE")) g->fvariant = atoi(fv);
+        int tya = 0, tyb = 0;
+        fused_tiles(g->fvariant, &tya, &tyb);
+        if (!tya) return bail(fail(PR_EINVAL, "fused variant %d is not built (PRK_VARIANTS)", g->fvariant));
+        g->f2 = (n % FusedP4::TXO == 0) && (n % tya == 0) && (n % tyb == 0) && !(fe && fe[0] == '0');
     }
     if (g->f2) {
         if ((s = setup_fused<K_A>(g)) != PR_OK) return bail(s);
@@ -877,7 +941,7 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
     }
     {
         const char *ce = getenv("PR_C2");
-        if (const char *cv = getenv("PR_CTILE")) g->cvariant = std::max(0, std::min(2, atoi(cv)));
+        if (const char *cv = getenv("PR_CTILE")) g->cvariant = atoi(cv);
         g->c2 = (n % CoarseP0::TXO == 0) && (n % CoarseP0::TYO == 0) && !(ce && ce[0] == '0');
     }
     if (g->c2 && (s = setup_coarse(g)) != PR_OK) return bail(s);
@@ -897,7 +961,7 @@ pr_status pr_destroy_grid(pr_grid *g) {
     if (!g) return PR_OK;
     cudaSetDevice(g->dev);
     cudaDeviceSynchronize();
-    for (auto &kv : g->graphs) cudaGraphExecDestroy(kv.second.first);
+    for (auto &kv : g->graphs) cudaGraphExecDestroy(kv.second.exec);
     g->graphs.clear();
     for (void *p : g->ipc_open) cudaIpcCloseMemHandle(p);
     cudaFree(g->d_flags); cudaFree(g->d_ipc);
@@ -908,6 +972,11 @@ pr_status pr_destroy_grid(pr_grid *g) {
     for (cudaStream_t t : g->slice_streams) cudaStreamDestroy(t);
     for (cudaEvent_t e : g->slice_events) cudaEventDestroy(e);
     if (g->comm) ncclCommDestroy(g->comm);
+    g->lgroup.reset();  // the last member's release destroys the group's events
+    cudaSetDevice(g->dev);
+    if (g->work_stream) cudaStreamDestroy(g->work_stream);
+    if (g->fork_ev) cudaEventDestroy(g->fork_ev);
+    if (g->join_ev) cudaEventDestroy(g->join_ev);
     for (double *p : g->pool) cudaFree(p);
     cudaFree(g->acc); cudaFree(g->ya); cudaFree(g->yb); cudaFree(g->ctmp);
     cudaFree(g->d_pos); cudaFree(g->d_red); cudaFree(g->d_sine);
@@ -927,16 +996,20 @@ pr_status pr_destroy_grid(pr_grid *g) {
 
 // G_c = prolong o (Alg.2 on the n/2 mesh) o restrict  (NEXT-4, C24-C26).
 // The n/2 mesh is a child grid with its own nu table, tiles and graphs.
+static pr_status ensure_half(pr_grid *g) {
+    if (g->half) return PR_OK;
+    pr_problem hp = g->prob;
+    hp.n = g->n / 2;
+    CKS(pr_create_grid(&hp, g->dev, &g->half));
+    const size_t m = size_t(g->n / 2);
+    CK(cudaMalloc(&g->half_u, m * m * m * sizeof(double)));
+    return PR_OK;
+}
+
 static pr_status run_coarse_mesh(pr_grid *g, const double *uin, double *uout, int64_t step0,
                                  int64_t nsteps, double dt, cudaStream_t st) {
     if (g->n % 4) return fail(PR_EINVAL, "coarse-mesh G needs n %% 4 == 0 (n = %d)", g->n);
-    if (!g->half) {
-        pr_problem hp = g->prob;
-        hp.n = g->n / 2;
-        CKS(pr_create_grid(&hp, g->dev, &g->half));
-        const size_t m = size_t(g->n / 2);
-        CK(cudaMalloc(&g->half_u, m * m * m * sizeof(double)));
-    }
+    CKS(ensure_half(g));
     const int blocks = g->sms * 8;
     restrict_kernel<<<blocks, 256, 0, st>>>(uin, g->half_u, g->n);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -1149,9 +1222,50 @@ pr_status pr_comm_init(pr_grid *g, int32_t world, int32_t rank, const void *id) 
         return fail(PR_ENCCL, "rank %d: ncclCommInitRank: %s", rank, ncclGetErrorString(r));
     }
     if (!g->comm_stream) CK(cudaStreamCreateWithFlags(&g->comm_stream, cudaStreamNonBlocking));
+    g->lgroup.reset();  // a communicator replaces an in-process rank group
     g->world = world;
     g->rank = rank;
     g->mapped_gen = -1;  // peer mappings belong to the previous communicator
+    return PR_OK;
+}
+
+pr_status pr_local_group(pr_grid **grids, int32_t world) {
+    if (!grids || world < 1) return fail(PR_EINVAL, "need grids and world >= 1");
+    for (int i = 0; i < world; ++i) {
+        if (!grids[i]) return fail(PR_EINVAL, "grid %d is NULL", i);
+        for (int j = 0; j < i; ++j)
+            if (grids[j] == grids[i]) return fail(PR_EINVAL, "grid %d appears twice", i);
+    }
+    auto grp = std::make_shared<LocalGroup>();
+    grp->r.resize(size_t(world));
+    for (int i = 0; i < world; ++i) grp->r[i].dev = grids[i]->dev;
+    // rank r's correction kernel stores into rank r+1's memory: peer access across devices
+    for (int i = 0; i + 1 < world; ++i) {
+        const int a = grids[i]->dev, b = grids[i + 1]->dev;
+        if (a == b) continue;
+        int ok = 0;
+        CK(cudaDeviceCanAccessPeer(&ok, a, b));
+        if (!ok) return fail(PR_EINVAL, "device %d cannot access device %d (peer access)", a, b);
+        CK(cudaSetDevice(a));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else CK(e);
+    }
+    for (int i = 0; i < world; ++i) {
+        pr_grid *g = grids[i];
+        CK(cudaSetDevice(g->dev));
+        if (g->comm) {
+            ncclCommDestroy(g->comm);
+            g->comm = nullptr;
+        }
+        if (!g->work_stream) CK(cudaStreamCreateWithFlags(&g->work_stream, cudaStreamNonBlocking));
+        if (!g->fork_ev) CK(cudaEventCreateWithFlags(&g->fork_ev, cudaEventDisableTiming));
+        if (!g->join_ev) CK(cudaEventCreateWithFlags(&g->join_ev, cudaEventDisableTiming));
+        g->lgroup = grp;
+        g->world = world;
+        g->rank = i;
+        g->seq_base = 0;
+    }
     return PR_OK;
 }
 
@@ -1164,10 +1278,17 @@ static pr_status ensure_events(pr_grid *g, size_t count) {
     return PR_OK;
 }
 
+// Seconds a rank waits for its predecessor's hand-off before it gives up with
+// PR_ENCCL (PR_NCCL_TIMEOUT_S; <= 0 waits forever).  Default 900 s: far above the
+// longest solve of BASELINE's configurations, finite so a stuck peer fails the call.
+static double handoff_timeout_s() {
+    const char *tenv = getenv("PR_NCCL_TIMEOUT_S");
+    return tenv ? atof(tenv) : 900.0;
+}
+
 // Wait for `st` (and the comm stream), polling NCCL for asynchronous errors.
 static pr_status wait_all(pr_grid *g, cudaStream_t st, int k_hint, bool with_comm = true) {
-    const char *tenv = getenv("PR_NCCL_TIMEOUT_S");
-    const double timeout = tenv ? atof(tenv) : 0.0;
+    const double timeout = handoff_timeout_s();
     const auto t0 = std::chrono::steady_clock::now();
     cudaStream_t ss[2] = {st, g->comm ? g->comm_stream : st};
     for (int i = 0; i < (with_comm ? 2 : 1); ++i) {
@@ -1176,6 +1297,13 @@ static pr_status wait_all(pr_grid *g, cudaStream_t st, int k_hint, bool with_com
             if (e == cudaSuccess) break;
             if (e != cudaErrorNotReady)
                 return fail(PR_ECUDA, "rank %d: stream error: %s", g->rank, cudaGetErrorString(e));
+            if (g->lgroup && timeout > 0) {  // in-process group: a peer that never delivers
+                const double el = std::chrono::duration<double>(
+                                      std::chrono::steady_clock::now() - t0).count();
+                if (el > timeout)
+                    return fail(PR_ENCCL, "rank %d, iteration %d: stream not done after %.1f s",
+                                g->rank, k_hint, el);
+            }
             if (g->comm) {
                 ncclResult_t ae = ncclSuccess;
                 ncclCommGetAsyncError(g->comm, &ae);
@@ -1274,12 +1402,74 @@ static pr_status peer_setup(pr_grid *g, double *mail_even, double *mail_odd) {
     return PR_OK;
 }
 
-static pr_status stream_wait_geq(cudaStream_t st, const unsigned int *addr, unsigned int v) {
-    CUresult e = stream_wait_fn()(reinterpret_cast<CUstream>(st),
-                                  reinterpret_cast<CUdeviceptr>(addr), v, CU_STREAM_WAIT_VALUE_GEQ);
+// The consumer side of a peer hand-off: the stream front end waits until the word the
+// peer publishes (st.release.sys after its data stores) reaches v.  The data arrived
+// over NVLink before the word, but a front-end wait is not an acquire: with
+// CU_STREAM_WAIT_VALUE_FLUSH (where the device supports it) the wait also flushes the
+// remote writes that preceded the word, and a one-thread ld.acquire.sys of the word +
+// fence.acq_rel.sys kernel orders every later kernel of the stream after them (the
+// value is already there, so it never spins).  cuda.h: CU_STREAM_WAIT_VALUE_FLUSH.
+static pr_status stream_wait_geq(pr_grid *g, cudaStream_t st, const unsigned int *addr, unsigned int v,
+                                 bool acquire) {
+    if (g->can_flush < 0) {
+        int f = 0;
+        if (cudaDeviceGetAttribute(&f, cudaDevAttrCanFlushRemoteWrites, g->dev) != cudaSuccess) {
+            cudaGetLastError();
+            f = 0;
+        }
+        g->can_flush = f ? 1 : 0;
+    }
+    const unsigned int flags = CU_STREAM_WAIT_VALUE_GEQ | (g->can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0);
+    CUresult e = stream_wait_fn()(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr),
+                                  v, flags);
     if (e != CUDA_SUCCESS) return fail(PR_ECUDA, "cuStreamWaitValue32 failed (%d)", int(e));
+    if (acquire) {
+        acquire_kernel<<<1, 1, 0, st>>>(addr);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        CKL();
+    }
     return PR_OK;
 }
+
+}  // extern "C"
+
+// ---- in-process rank group (pr_local_group): host-side announcements
+// Block until pred() holds for the group state, or fail with PR_ENCCL after the
+// hand-off timeout (a stuck or failed peer rank).
+template <class Pred>
+static pr_status local_wait(pr_grid *g, int k, int peer, const char *what, Pred pred) {
+    LocalGroup &G = *g->lgroup;
+    const double tmo = handoff_timeout_s();
+    std::unique_lock<std::mutex> lk(G.mu);
+    const auto t0 = std::chrono::steady_clock::now();
+    while (!pred(G)) {
+        if (tmo > 0) {
+            const auto until = t0 + std::chrono::duration_cast<std::chrono::steady_clock::duration>(
+                                        std::chrono::duration<double>(tmo));
+            if (G.cv.wait_until(lk, until) == std::cv_status::timeout && !pred(G))
+                return fail(PR_ENCCL, "rank %d, iteration %d: timed out after %.1f s waiting for rank %d (%s)",
+                            g->rank, k, tmo, peer, what);
+        } else {
+            G.cv.wait(lk);
+        }
+    }
+    return PR_OK;
+}
+
+// record `ev` on st, then publish `field = v` of this rank under the group lock
+static pr_status local_publish(pr_grid *g, cudaEvent_t ev, cudaStream_t st,
+                               unsigned long long LocalRank::*field, unsigned long long v) {
+    if (ev) CK(cudaEventRecord(ev, st));
+    LocalGroup &G = *g->lgroup;
+    {
+        std::lock_guard<std::mutex> lk(G.mu);
+        G.r[g->rank].*field = v;
+    }
+    G.cv.notify_all();
+    return PR_OK;
+}
+
+extern "C" {
 
 static pr_status post(pr_grid *g, double *stop_dst, double stop, unsigned int *flag, unsigned int seq,
                       cudaStream_t st) {
@@ -1333,13 +1523,20 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
     const bool ctrl = tol > 0.0;  // convergence-controlled stopping (C23)
     if (Np < 1 || nc < 1 || nf < 1 || K < 0 || !(tol == tol))
         return fail(PR_EINVAL, "need n_slices, N_c, N_f >= 1, K >= 0 and a number for tol");
-    const int W = g->comm ? g->world : 1, r = g->comm ? g->rank : 0;
-    if (g->world > 1 && !g->comm) return fail(PR_ESTATE, "world > 1 but no communicator");
+    const bool local = g->lgroup != nullptr;  // in-process rank group (pr_local_group)
+    const int W = (g->comm || local) ? g->world : 1, r = (g->comm || local) ? g->rank : 0;
+    if (g->world > 1 && !g->comm && !local) return fail(PR_ESTATE, "world > 1 but no communicator");
     if (Np % W) return fail(PR_EINVAL, "n_slices (%d) must be a multiple of world (%d)", Np, W);
     const bool last = (r == W - 1);
     if (last && !u_T) return fail(PR_EINVAL, "u_T is NULL on the last rank");
     const int s = Np / W, j0 = r * s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaStream_t user_st = st;
+    if (local) {  // each rank of a group runs on its grid's own stream, joined to the caller's
+        CK(cudaEventRecord(g->fork_ev, user_st));
+        st = g->work_stream;
+        CK(cudaStreamWaitEvent(st, g->fork_ev, 0));
+    }
     const double T = g->prob.T;
     const double Dt = T / double(int64_t(Np) * nc);  // coarse step
     const double dt = T / double(int64_t(Np) * nf);  // fine step
@@ -1375,12 +1572,34 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
     double *gnew = g->pool[4 * s], *recvb = g->pool[4 * s + 1], *u0d = g->pool[4 * s + 2];
     // peer hand-off: the receive buffer alternates between pool[4s+1] (even k) and
     // pool[0] (odd k: start[0] swaps with recvb at the end of every iteration)
-    const bool peer = (cfg->flags & PR_FLAG_PEER_HANDOFF) && W > 1;
+    const bool lh = local && W > 1;  // in-process hand-off (events announced through the group)
+    const bool peer = (cfg->flags & PR_FLAG_PEER_HANDOFF) && W > 1 && !local;
     unsigned int base = 0;
     if (peer) {
         CKS(peer_setup(g, g->pool[4 * s + 1], g->pool[0]));
         base = g->seq_base;
         g->seq_base += unsigned(K) + 2;
+    }
+    LocalGroup *LG = lh ? g->lgroup.get() : nullptr;
+    if (lh) {
+        base = g->seq_base;
+        g->seq_base += unsigned(K) + 2;
+        {  // this call's receive buffers (idle until its first receive) and event slots
+            std::lock_guard<std::mutex> lk(LG->mu);
+            LocalRank &me = LG->r[r];
+            while (me.ev_data.size() < size_t(std::max(K, 1))) {
+                cudaEvent_t a, b;
+                CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+                me.ev_data.push_back(a);
+                me.ev_free.push_back(b);
+            }
+            me.mail[0] = g->pool[4 * s + 1];
+            me.mail[1] = g->pool[0];
+            me.freed = base;
+            me.started = base + 1ull;
+        }
+        LG->cv.notify_all();
     }
     const bool want_def = last && u_ref && defects_host;
     const double *refd = u_ref;
@@ -1421,7 +1640,12 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
         CKS(ensure_table(g, 1, dt, 0, int64_t(j0 + s) * nf, st));
     } else {
         CKS(ensure_table(g, 1, dt, int64_t(j0) * nf, int64_t(j0 + s) * nf, st));
-        CKS(ensure_table(g, 0, Dt, 0, int64_t(j0 + s) * nc, st));
+        if (g_half) {  // G_c runs on the n/2 child grid: its table, once, for all slices
+            CKS(ensure_half(g));
+            CKS(ensure_table(g->half, 0, Dt, 0, int64_t(j0 + s) * nc, st));
+        } else {
+            CKS(ensure_table(g, 0, Dt, 0, int64_t(j0 + s) * nc, st));
+        }
     }
     // slots: d_red[k] = max|u^k_{N_p} - u_ref| (k = 0..K), d_red[K+1] = max|u_ref|
     if (want_def) CKS(launch_maxabs(g, nullptr, refd, nullptr, g->d_red + K + 1, st));
@@ -1485,6 +1709,9 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
             // peer mode: start[0] (next iteration's receive buffer of the same parity) is free
             if (peer && r > 0 && (conc ? l == s - 1 : l == 0))
                 CKS(post(g, nullptr, 0.0, g->pred_flags + 1, base + unsigned(op.k) + 1, st));
+            if (lh && r > 0 && (conc ? l == s - 1 : l == 0))
+                CKS(local_publish(g, LG->r[r].ev_free[op.k], st, &LocalRank::freed,
+                                  base + unsigned(op.k) + 1ull));
             if (l == s - 1) {
                 CK(cudaEventRecord(evF(op.k), st));
                 CK(cudaEventRecord(fdone_ev, st));
@@ -1494,7 +1721,22 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
             recvd = false;
             if (pred_stopped) break;  // the predecessor sent its last message earlier
             if (peer) {  // the predecessor's correction stored straight into recvb
-                CKS(stream_wait_geq(st, g->d_flags + 0, base + unsigned(op.k) + 1));
+                CKS(stream_wait_geq(g, st, g->d_flags + 0, base + unsigned(op.k) + 1, true));
+                if (ctrl) CK(cudaMemcpyAsync(g->h_flag, recvb + g->N, sizeof(double),
+                                             cudaMemcpyDeviceToHost, st));
+                recvd = true;
+                break;
+            }
+            if (lh) {  // same data path; order after the predecessor's announced event
+                const unsigned long long want = base + unsigned(op.k) + 1ull;
+                CKS(local_wait(g, op.k, r - 1, "its hand-off",
+                               [&](LocalGroup &G_) { return G_.r[r - 1].data >= want; }));
+                cudaEvent_t ev;
+                {
+                    std::lock_guard<std::mutex> lk(LG->mu);
+                    ev = LG->r[r - 1].ev_data[op.k];
+                }
+                CK(cudaStreamWaitEvent(st, ev, 0));
                 if (ctrl) CK(cudaMemcpyAsync(g->h_flag, recvb + g->N, sizeof(double),
                                              cudaMemcpyDeviceToHost, st));
                 recvd = true;
@@ -1531,8 +1773,25 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
             // receive buffer once the successor has released it
             double *pmail = nullptr;
             if (peer && l == s - 1 && r < W - 1) {
-                CKS(stream_wait_geq(st, g->d_flags + 1, base + unsigned(op.k)));
+                CKS(stream_wait_geq(g, st, g->d_flags + 1, base + unsigned(op.k), false));
                 pmail = g->peer_mail[op.k & 1];
+            }
+            if (lh && l == s - 1 && r < W - 1) {  // the successor has released the buffer
+                const int k = op.k;
+                if (k == 0) {
+                    CKS(local_wait(g, k, r + 1, "the start of its call",
+                                   [&](LocalGroup &G_) { return G_.r[r + 1].started >= base + 1ull; }));
+                } else {
+                    CKS(local_wait(g, k, r + 1, "its receive buffer",
+                                   [&](LocalGroup &G_) { return G_.r[r + 1].freed >= base + unsigned(k); }));
+                }
+                cudaEvent_t ev = nullptr;
+                {
+                    std::lock_guard<std::mutex> lk(LG->mu);
+                    if (k > 0) ev = LG->r[r + 1].ev_free[k - 1];
+                    pmail = LG->r[r + 1].mail[k & 1];
+                }
+                if (ev) CK(cudaStreamWaitEvent(st, ev, 0));
             }
             CKS(launch_correct(g, f[l], gnew, gold[l], out[l], fuse ? refd : nullptr,
                                g->d_red + op.k + 1, st, prev, red_chg + 2 * op.k,
@@ -1550,7 +1809,7 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
                     g->monitors[op.k] = ch;
                     if (recvd && g->h_flag[0] != 0.0) pred_stopped = true;
                     if (pred_stopped && ch <= tol) stop_now = true;
-                    if (r < W - 1 && !peer) {  // the flag rides on this iteration's message
+                    if (r < W - 1 && !peer && !lh) {  // the flag rides on this iteration's message
                         set_flag_kernel<<<1, 1, 0, st>>>(out[s - 1] + g->N, stop_now ? 1.0 : 0.0);
                         g_launches.fetch_add(1, std::memory_order_relaxed);
                         CKL();
@@ -1559,12 +1818,21 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
                 if (peer && r < W - 1)  // publish: stop flag, then the data sequence word
                     CKS(post(g, ctrl ? pmail + g->N : nullptr, stop_now ? 1.0 : 0.0,
                              g->succ_flags + 0, base + unsigned(op.k) + 1, st));
+                if (lh && r < W - 1) {  // stop flag into the message tail, then announce
+                    if (ctrl) {
+                        set_flag_kernel<<<1, 1, 0, st>>>(pmail + g->N, stop_now ? 1.0 : 0.0);
+                        g_launches.fetch_add(1, std::memory_order_relaxed);
+                        CKL();
+                    }
+                    CKS(local_publish(g, LG->r[r].ev_data[op.k], st, &LocalRank::data,
+                                      base + unsigned(op.k) + 1ull));
+                }
                 if (stop_now) stopped = true;
             }
             break;
         }
         case PR_OP_SEND:
-            if (peer) break;  // stored by the correction kernel, published by post_kernel
+            if (peer || lh) break;  // stored by the correction kernel, then published
             CK(cudaEventRecord(corr_ev(op.k), st));
             CK(cudaStreamWaitEvent(g->comm_stream, corr_ev(op.k), 0));
             NCK(ncclSend(out[s - 1], msg, ncclDouble, op.peer, g->comm, g->comm_stream), op.k);
@@ -1583,7 +1851,7 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
         }
         // a rank that stops still sends its last message (and records its iteration end)
         if (stopped && op.op == PR_OP_CORRECT && op.slice == j0 + s - 1) {
-            if (r < W - 1 && !peer) {
+            if (r < W - 1 && !peer && !lh) {
                 CK(cudaEventRecord(corr_ev(op.k), st));
                 CK(cudaStreamWaitEvent(g->comm_stream, corr_ev(op.k), 0));
                 NCK(ncclSend(out[s - 1], msg, ncclDouble, r + 1, g->comm, g->comm_stream), op.k);
@@ -1604,6 +1872,10 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
                        cudaMemcpyDeviceToHost, st));
     cudaEvent_t ev_end = g->evs[2 + 4 * K];
     CK(cudaEventRecord(ev_end, st));
+    if (local) {
+        CK(cudaEventRecord(g->join_ev, st));
+        CK(cudaStreamWaitEvent(user_st, g->join_ev, 0));
+    }
     CKS(wait_all(g, st, K - 1));
     if (want_def) {
         const double M = bits_to_double(g->h_red[K + 1]);

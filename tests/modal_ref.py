@@ -163,6 +163,20 @@ def synthesize(n, thetas, amps):
     return out
 
 
+def synthesize_torch(n, thetas, amps, device):
+    """synthesize() evaluated with torch on `device` (large n: 512^3 in seconds).
+    Same formula, fp64; a checker, not part of the CUDA path."""
+    import torch
+    idx = torch.arange(n, dtype=torch.float64, device=device)
+    out = torch.zeros((n, n, n), dtype=torch.float64, device=device)
+    for th, a in zip(thetas, amps):
+        ex = torch.exp(1j * float(th[0]) * idx)
+        ey = torch.exp(1j * float(th[1]) * idx)
+        ez = torch.exp(1j * float(th[2]) * idx)
+        out += torch.real(complex(a) * ez[:, None, None] * ey[None, :, None] * ex[None, None, :])
+    return out
+
+
 def exact_solution(n, c, nu0, omega, t):
     """Closed form u = a(t) u0(x - c t) (exp restored per C18)."""
     a = np.exp(-12.0 * np.pi ** 2 * nu_integral(nu0, omega, t))

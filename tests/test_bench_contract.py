@@ -55,4 +55,12 @@ def test_bench_json_on_gpu():
         assert k in d["roofline"], k
     assert d["gpu_launches"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    # the timed solve checks itself against the exact modal recurrence
+    assert d["parity"]["ok"], d["parity"]
+    assert d["parity"]["max_abs_dk_vs_modal"] <= 1e-10 and d["parity"]["u_T_rel_err_vs_modal"] <= 1e-12
+    assert d["roofline"]["within_peak"]
+    # the reference arm reports the same workload config
+    ref = run(["--impl", "reference", "--config", "cfg1", "--steps", "1", "--warmup", "0"])
+    r = json.loads([l for l in ref.stdout.splitlines() if l.startswith("{")][-1])
+    assert r["config"] == d["config"]
 

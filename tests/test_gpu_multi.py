@@ -47,3 +47,18 @@ def test_parareal_multi_gpu(W, n, Np, K, tol, handoff):
     assert res.returncode == 0 and lines, res.stdout[-3000:] + res.stderr[-3000:]
     info = json.loads(lines[-1])
     assert info["ok"] and info["bitwise_equal_to_1gpu"], info
+
+
+@pytest.mark.parametrize("handoff", ["nccl"])
+def test_stuck_predecessor_nccl(handoff):
+    """Rank 0 never sends: rank 1's pr_parareal returns PR_ENCCL with its rank and
+    iteration after PR_NCCL_TIMEOUT_S (tools/mgpu_stuck.py)."""
+    if ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "tools", "mgpu_stuck.py"), handoff]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert res.returncode == 0 and lines, res.stdout[-3000:] + res.stderr[-3000:]
+    assert json.loads(lines[-1])["ok"]

@@ -234,7 +234,7 @@ def test_fine_paths_agree(n, f2, monkeypatch):
     g.destroy()
 
 
-@pytest.mark.parametrize("variant", [str(v) for v in range(10, 20)])
+@pytest.mark.parametrize("variant", [str(v) for v in range(10, 22)])
 def test_fused_variants_bitwise(variant, monkeypatch):
     """Every persistent fused tile variant (PR_FTILE) gives the four-stage
     path's bits: same folded weights, same operation order per point.  n = 128
@@ -247,7 +247,7 @@ def test_fused_variants_bitwise(variant, monkeypatch):
         monkeypatch.setenv("PR_FTILE", v)
         try:
             g = pr.Grid(pr.Problem(n, c=PARITY_C))
-        except pr.PrError as e:  # a tuning variant that does not fit this GPU
+        except pr.PrError as e:  # a tuning variant not built (PRK_VARIANTS) or not fitting
             pytest.skip(str(e))
         out = torch.empty_like(u0)
         pr.pr_fine(g, u0, out, 3, 21, 1e-4)
@@ -385,7 +385,10 @@ def test_coarse_kernels_bitwise(n, variant, monkeypatch):
     for c2 in ("0", "1"):
         monkeypatch.setenv("PR_C2", c2)
         monkeypatch.setenv("PR_CTILE", variant)
-        g = pr.Grid(pr.Problem(n, c=PARITY_C))
+        try:
+            g = pr.Grid(pr.Problem(n, c=PARITY_C))
+        except pr.PrError as e:  # a tuning variant not built (PRK_VARIANTS)
+            pytest.skip(str(e))
         out = torch.empty_like(u0)
         pr.pr_coarse(g, u0, out, 5, 37, 4e-4 * (32 / n) ** 2)
         outs.append(out)
