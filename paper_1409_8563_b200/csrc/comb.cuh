@@ -16,8 +16,10 @@
 // The extended ring of stage A (2 points around the tile) is computed by two
 // "ring" warps that do stage A only.  Per tile plane: stage B of output plane m
 // runs in iteration j = m + 5 (its intermediate planes m..m+4 are all done),
-// then stage A of plane j; one named barrier over the compute warps per
-// iteration orders the intermediate ring (4 slots).  Producer warps and the
+// then stage A of plane j; the intermediate ring (ZD slots) is ordered by
+// mbarrier pairs (full: every compute lane wrote the plane; empty: every
+// combined lane read its neighbours in it), so warps drift up to ZD-4 planes
+// apart instead of running in lockstep.  Producer warps and the
 // input ring are those of fused.cuh (TMA tensor fills, cp.async on seams).
 // Same per-point floating-point operation sequence as the four-pass kernels:
 // the results are bitwise identical.
@@ -52,15 +54,12 @@ struct CombCfg {
                                  size_t(ZD) * Z_ELEMS);
     }
 };
-using Comb16 = CombCfg<16, 9>;  // 32x16 tile: 4 combined + 2 ring + 2 producer warps
-
-__device__ __forceinline__ void bar_compute(int nthreads) {
-    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
-}
+using Comb16 = CombCfg<16, 9, 2, 2, 6>;  // 32x16 tile: 4 combined + 2 ring + 2 producer warps
 
 template <int KB, class C>
 __device__ __forceinline__ void comb_consumer(const StencilArgs &a, double *sm, int items,
-                                              uint64_t *in_full, uint64_t *in_empty) {
+                                              uint64_t *in_full, uint64_t *in_empty, uint64_t *zfull,
+                                              uint64_t *zempty) {
     constexpr int RPT = C::RPT, DEPTH = C::DEPTH, EW = C::EWS, IW = C::IWS, TXO = C::TXO, ZD = C::ZD;
     double *yring = sm;
     double *aring = yring + size_t(DEPTH) * C::Y_ELEMS;
@@ -105,20 +104,19 @@ __device__ __forceinline__ void comb_consumer(const StencilArgs &a, double *sm, 
     WA.set(a.nu_tab[row + (KB == K_A ? 0 : 2)], a.inv_dx, a.c);
     WB.set(a.nu_tab[row + (KB == K_A ? 1 : 3)], a.inv_dx, a.c);
     const double dt = a.dt;
-    constexpr int NC = C::NTA;
 
     RingPos base;  // input element 0 of the current item
-    int zj = 0;    // intermediate ring slot of plane j (runs on across items)
+    RingPos zw;    // intermediate ring: position of the plane stage A writes next
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const WorkItem w = decode_item(a, item, TXO, C::TYO);
-        const int NJ = w.nz + 4;
+        const int NJ = w.nz + 4;  // >= 5
         double *o0 = a.o0 + size_t(w.z_begin) * nn + size_t(w.y0 + r0 - 2) * n + w.x0 + 2 * l - 2;
         double *o1 = KB == K_A ? a.o1 + size_t(w.z_begin) * nn + size_t(w.y0 + r0 - 2) * n + w.x0 + 2 * l - 2
                                : nullptr;
-        double2 qa[RPT][5];  // input z-queue
-        double2 qb[RPT][5];  // own intermediate values, planes j-5 .. j-1
-        double2 tl[3][RPT];  // t0 of planes j-3, j-2, j-1
+        double2 qa[RPT][5];  // input z-queue: element e at index e % 5 (e = j .. j+4 in iteration j)
+        double2 qb[RPT][5];  // own intermediate values: plane p at index p % 5
+        double2 tq[RPT][5];  // own t0 values: plane p at index p % 5
         RingPos p0 = base;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -131,97 +129,185 @@ __device__ __forceinline__ void comb_consumer(const StencilArgs &a, double *sm, 
         mbar_arrive(&in_empty[base.slot]);
         mbar_arrive(&in_empty[ring_at(base, 1, DEPTH).slot]);
         RingPos p2 = ring_at(base, 2, DEPTH), p4 = p0;  // elements j+2, j+4
-        // iteration j: stage B of output plane j-5 (j >= 5), then stage A of plane j (j < NJ)
-        rotating_loop(NJ + 1, [&](auto ph, int j) {
-            constexpr int P = decltype(ph)::value;  // qa[.][(P+k)%5] = element j+k-1 before the load
-            if (comb && j >= 5) {
-                // x/y neighbours of intermediate plane j-3 (the centre of output j-5)
-                const int zc = zj >= 3 ? zj - 3 : zj - 3 + ZD;
-                const double *zp = zring + size_t(zc) * C::Z_ELEMS + sZ;
-                double2 col[RPT + 4];
+        RingPos zr = zw;  // intermediate ring: plane j-3 (stage B's centre in iteration j >= 5)
+
+        // ---- the pieces of one iteration j (phase P = j % 5)
+        // stage A loads: element j+4 into the z-queue, x/y neighbours of element j+2, aux j
+        struct ALd { double2 col[RPT + 4], xl[RPT], xr[RPT], ub[RPT], ac[RPT]; };
+        auto a_load = [&](auto ph, ALd &L) {
+            constexpr int P = decltype(ph)::value;
+            const double *yq = yring + size_t(p4.slot) * C::Y_ELEMS + sY;
 #pragma unroll
-                for (int r = 0; r < RPT + 4; ++r)
-                    col[r] = (r >= 2 && r < RPT + 2) ? qb[r - 2][(P + 2) % 5] : lds2(zp + (r - 2) * EW);
+            for (int r = 0; r < RPT; ++r) qa[r][(P + 4) % 5] = lds2(yq + r * IW);
+            const double *ys = yring + size_t(p2.slot) * C::Y_ELEMS + sY;
 #pragma unroll
-                for (int r = 0; r < RPT; ++r) {
-                    const double2 kB = apply_pair<P>(WB, lds2(zp + r * EW - 2), lds2(zp + r * EW + 2), col[r],
-                                                     col[r + 1], col[r + 3], col[r + 4], qb[r]);
-                    const size_t gofs = size_t(r) * n;
-                    const double2 t0 = tl[0][r];
-                    if (KB == K_A) {
-                        const double2 t1 = qa[r][(P + 4) % 5];  // u at the output point (element j-1)
-                        double2 v0, v1;
-                        v0.x = t0.x + (dt / 3.0) * kB.x;  v0.y = t0.y + (dt / 3.0) * kB.y;
-                        v1.x = t1.x + (dt / 2.0) * kB.x;  v1.y = t1.y + (dt / 2.0) * kB.y;
-                        *reinterpret_cast<double2 *>(o0 + gofs) = v0;
-                        *reinterpret_cast<double2 *>(o1 + gofs) = v1;
-                    } else {
-                        double2 v0;
-                        v0.x = t0.x + (dt / 6.0) * kB.x;  v0.y = t0.y + (dt / 6.0) * kB.y;
-                        *reinterpret_cast<double2 *>(o0 + gofs) = v0;
-                    }
-                }
-                o0 += nn;
-                if (KB == K_A) o1 += nn;
+            for (int r = 0; r < RPT + 4; ++r)
+                L.col[r] = (r >= 2 && r < RPT + 2) ? qa[r - 2][(P + 2) % 5] : lds2(ys + (r - 2) * IW);
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                L.xl[r] = lds2(ys + r * IW - 2);
+                L.xr[r] = lds2(ys + r * IW + 2);
             }
-            if (j < NJ) {
-                mbar_wait(&in_full[p4.slot], p4.round & 1);  // element j+4 (+ aux j) landed
-                const double *yq = yring + size_t(p4.slot) * C::Y_ELEMS + sY;
-#pragma unroll
-                for (int r = 0; r < RPT; ++r) qa[r][(P + 4) % 5] = lds2(yq + r * IW);
-                const double *ys = yring + size_t(p2.slot) * C::Y_ELEMS + sY;
-                double2 col[RPT + 4];
-#pragma unroll
-                for (int r = 0; r < RPT + 4; ++r)
-                    col[r] = (r >= 2 && r < RPT + 2) ? qa[r - 2][(P + 2) % 5] : lds2(ys + (r - 2) * IW);
+            if constexpr (KB == K_B) {
                 const double *au = aring + size_t(p4.slot) * C::AUX_ELEMS;  // aux j
-                double2 ubv[KB == K_B ? RPT : 1], acv[KB == K_B ? RPT : 1];
-                if constexpr (KB == K_B) {
-#pragma unroll
-                    for (int r = 0; r < RPT; ++r) {
-                        ubv[r] = lds2(au + sZ + r * EW);
-                        acv[r] = lds2(au + C::Z_ELEMS + (comb ? tp0 + r * TXO : 0));
-                    }
-                } else {
-                    (void)au;
-                }
-                double2 k[RPT];
-#pragma unroll
-                for (int r = 0; r < RPT; ++r)
-                    k[r] = apply_pair<P>(WA, lds2(ys + r * IW - 2), lds2(ys + r * IW + 2), col[r], col[r + 1],
-                                         col[r + 3], col[r + 4], qa[r]);
-                double *zd = zring + size_t(zj) * C::Z_ELEMS + sZ;
 #pragma unroll
                 for (int r = 0; r < RPT; ++r) {
-                    const double2 yc = qa[r][(P + 2) % 5];
-                    double2 z, t0;
-                    if (KB == K_A) {
-                        z.x = yc.x + (dt / 2.0) * k[r].x;
-                        z.y = yc.y + (dt / 2.0) * k[r].y;
-                        t0.x = yc.x + (dt / 6.0) * k[r].x;
-                        t0.y = yc.y + (dt / 6.0) * k[r].y;
-                    } else {
-                        const double2 ub = ubv[KB == K_B ? r : 0], ac = acv[KB == K_B ? r : 0];
-                        z.x = ub.x + dt * k[r].x;
-                        z.y = ub.y + dt * k[r].y;
-                        t0.x = ac.x + (dt / 3.0) * k[r].x;
-                        t0.y = ac.y + (dt / 3.0) * k[r].y;
-                    }
-                    if (valid) sts2(zd + r * EW, z);
-                    if (comb) {
-                        qb[r][P] = z;  // plane j replaces plane j-5
-                        tl[0][r] = tl[1][r];
-                        tl[1][r] = tl[2][r];
-                        tl[2][r] = t0;
-                    }
+                    L.ub[r] = lds2(au + sZ + r * EW);
+                    L.ac[r] = lds2(au + C::Z_ELEMS + (comb ? tp0 + r * TXO : 0));
                 }
-                mbar_arrive(&in_empty[p2.slot]);  // element j+2 done (aux j lives in slot j+4)
-                p2.step(DEPTH);
-                p4.step(DEPTH);
             }
-            zj = (zj + 1 == ZD) ? 0 : zj + 1;
-            bar_compute(NC);
-        });
+        };
+        // stage A compute (registers only)
+        struct K2 { double2 k[RPT]; };
+        auto a_compute = [&](auto ph, const ALd &L, K2 &K) {
+            constexpr int P = decltype(ph)::value;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r)
+                K.k[r] = apply_pair<P>(WA, L.xl[r], L.xr[r], L.col[r], L.col[r + 1], L.col[r + 3], L.col[r + 4],
+                                       qa[r]);
+        };
+        // stage A results: the intermediate plane j (ring and own queue) and t0
+        auto a_store = [&](auto ph, const ALd &L, const K2 &K) {
+            constexpr int P = decltype(ph)::value;
+            mbar_arrive(&in_empty[p2.slot]);  // element j+2 done (aux j lives in slot j+4)
+            if (zw.round > 0) mbar_wait(&zempty[zw.slot], (zw.round - 1) & 1);
+            double *zd = zring + size_t(zw.slot) * C::Z_ELEMS + sZ;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                const double2 yc = qa[r][(P + 2) % 5];
+                double2 z, t0;
+                if (KB == K_A) {
+                    z.x = yc.x + (dt / 2.0) * K.k[r].x;
+                    z.y = yc.y + (dt / 2.0) * K.k[r].y;
+                    t0.x = yc.x + (dt / 6.0) * K.k[r].x;
+                    t0.y = yc.y + (dt / 6.0) * K.k[r].y;
+                } else {
+                    z.x = L.ub[r].x + dt * K.k[r].x;
+                    z.y = L.ub[r].y + dt * K.k[r].y;
+                    t0.x = L.ac[r].x + (dt / 3.0) * K.k[r].x;
+                    t0.y = L.ac[r].y + (dt / 3.0) * K.k[r].y;
+                }
+                if (valid) sts2(zd + r * EW, z);
+                qb[r][P] = z;  // plane j replaces plane j-5
+                tq[r][P] = t0;
+            }
+            mbar_arrive(&zfull[zw.slot]);
+            zw.step(ZD);
+            p2.step(DEPTH);
+            p4.step(DEPTH);
+        };
+        // stage B loads: x/y neighbours of intermediate plane j-3 (centre of output j-5)
+        struct BLd { double2 col[RPT + 4], xl[RPT], xr[RPT], t1[RPT]; };
+        auto b_load = [&](auto ph, BLd &L) {
+            constexpr int P = decltype(ph)::value;
+            const double *zp = zring + size_t(zr.slot) * C::Z_ELEMS + sZ;
+#pragma unroll
+            for (int r = 0; r < RPT + 4; ++r)
+                L.col[r] = (r >= 2 && r < RPT + 2) ? qb[r - 2][(P + 2) % 5] : lds2(zp + (r - 2) * EW);
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                L.xl[r] = lds2(zp + r * EW - 2);
+                L.xr[r] = lds2(zp + r * EW + 2);
+                L.t1[r] = qa[r][(P + 4) % 5];  // u at the output point (element j-1), before a_load
+            }
+        };
+        // stage B compute (registers only)
+        auto b_compute = [&](auto ph, const BLd &L, K2 &K) {
+            constexpr int P = decltype(ph)::value;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r)
+                K.k[r] = apply_pair<P>(WB, L.xl[r], L.xr[r], L.col[r], L.col[r + 1], L.col[r + 3], L.col[r + 4],
+                                       qb[r]);
+        };
+        // stage B results: output plane j-5 to HBM
+        auto b_store = [&](auto ph, const BLd &L, const K2 &K) {
+            constexpr int P = decltype(ph)::value;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                const double2 kB = K.k[r];
+                const size_t gofs = size_t(r) * n;
+                const double2 t0 = tq[r][(P + 2) % 5];
+                if (KB == K_A) {
+                    const double2 t1 = L.t1[r];
+                    double2 v0, v1;
+                    v0.x = t0.x + (dt / 3.0) * kB.x;  v0.y = t0.y + (dt / 3.0) * kB.y;
+                    v1.x = t1.x + (dt / 2.0) * kB.x;  v1.y = t1.y + (dt / 2.0) * kB.y;
+                    *reinterpret_cast<double2 *>(o0 + gofs) = v0;
+                    *reinterpret_cast<double2 *>(o1 + gofs) = v1;
+                } else {
+                    double2 v0;
+                    v0.x = t0.x + (dt / 6.0) * kB.x;  v0.y = t0.y + (dt / 6.0) * kB.y;
+                    *reinterpret_cast<double2 *>(o0 + gofs) = v0;
+                }
+            }
+            o0 += nn;
+            if (KB == K_A) o1 += nn;
+            mbar_arrive(&zempty[zr.slot]);  // plane j-3 read
+            zr.step(ZD);
+        };
+        // release a plane stage B never reads (0, 1, NJ-2, NJ-1) -- only once every lane has
+        // written it: an early release could complete the slot's empty phase twice before
+        // a slow writer waits on it (its parity wait would then never return)
+        auto release_unread = [&]() {
+            mbar_wait(&zfull[zr.slot], zr.round & 1);
+            mbar_arrive(&zempty[zr.slot]);
+            zr.step(ZD);
+        };
+        auto stage_a = [&](auto ph) {
+            mbar_wait(&in_full[p4.slot], p4.round & 1);  // element j+4 (+ aux j) landed
+            ALd L;
+            K2 K;
+            a_load(ph, L);
+            a_compute(ph, L, K);
+            a_store(ph, L, K);
+        };
+        auto stage_b = [&](auto ph) {
+            mbar_wait(&zfull[zr.slot], zr.round & 1);
+            BLd L;
+            K2 K;
+            b_load(ph, L);
+            b_compute(ph, L, K);
+            b_store(ph, L, K);
+        };
+
+        if (comb) {
+            // j = 0 .. 4: stage A only; intermediate planes 0 and 1 are never a centre
+            stage_a(Ph<0>{});
+            stage_a(Ph<1>{});
+            stage_a(Ph<2>{});
+            release_unread();
+            stage_a(Ph<3>{});
+            release_unread();
+            stage_a(Ph<4>{});
+            // j = 5 .. NJ-1: both stages; every wait first, then both stages' loads, so the
+            // two dependency chains of the iteration overlap
+            rotating_loop(NJ - 5, [&](auto ph, int) {
+                mbar_wait(&zfull[zr.slot], zr.round & 1);
+                mbar_wait(&in_full[p4.slot], p4.round & 1);
+                BLd LB;
+                ALd LA;
+                K2 KB_, KA_;
+                b_load(ph, LB);
+                a_load(ph, LA);
+                b_compute(ph, LB, KB_);
+                a_compute(ph, LA, KA_);
+                b_store(ph, LB, KB_);
+                a_store(ph, LA, KA_);
+            });
+            // j = NJ: stage B of the last output plane
+            switch (NJ % 5) {
+            case 0: stage_b(Ph<0>{}); break;
+            case 1: stage_b(Ph<1>{}); break;
+            case 2: stage_b(Ph<2>{}); break;
+            case 3: stage_b(Ph<3>{}); break;
+            default: stage_b(Ph<4>{}); break;
+            }
+            // the item's last two intermediate planes are never a centre
+            release_unread();
+            release_unread();
+        } else {  // ring lanes: stage A on the extended ring only
+            rotating_loop(NJ, [&](auto ph, int) { stage_a(ph); });
+        }
         // the item's last two input elements were only used by the queue
         mbar_arrive(&in_empty[p2.slot]);
         mbar_arrive(&in_empty[ring_at(p2, 1, DEPTH).slot]);
@@ -233,7 +319,7 @@ template <int KB, class C>
 __global__ void __maxnreg__(C::MAXR)
 fused_comb_kernel(const StencilArgs a, const __grid_constant__ TmaMaps tm) {
     extern __shared__ __align__(128) double sm[];
-    __shared__ __align__(8) uint64_t in_full[C::DEPTH], in_empty[C::DEPTH];
+    __shared__ __align__(8) uint64_t in_full[C::DEPTH], in_empty[C::DEPTH], zfull[C::ZD], zempty[C::ZD];
     const int items = a.tiles_x * a.tiles_y * a.chunks_z;
     if constexpr (C::FILL == 2) {
         if (smem_u32(sm) & 127) __trap();  // TMA destinations need 128-byte alignment
@@ -243,11 +329,15 @@ fused_comb_kernel(const StencilArgs a, const __grid_constant__ TmaMaps tm) {
             mbar_init(&in_full[s], C::NTP);
             mbar_init(&in_empty[s], C::NTA);
         }
+        for (int s = 0; s < C::ZD; ++s) {
+            mbar_init(&zfull[s], C::NTA);   // every compute thread wrote its part of the plane
+            mbar_init(&zempty[s], C::NTC);  // every combined thread read its neighbours in it
+        }
         fence_mbar_init();
     }
     __syncthreads();
     if (threadIdx.x < C::NTA)
-        comb_consumer<KB, C>(a, sm, items, in_full, in_empty);
+        comb_consumer<KB, C>(a, sm, items, in_full, in_empty, zfull, zempty);
     else
         producer_p<KB, C>(a, &tm, sm, items, in_full, in_empty);
 }

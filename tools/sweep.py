@@ -1,8 +1,9 @@
 """Coarse/fine ratio and K sweep at 256^3 (BASELINE configs[4]) on W GPUs.
 
     python tools/sweep.py W out.jsonl [--handoff peer]
-Runs bench.py under torchrun for N_t in {2^12, 2^13, 2^14} (N_C = 2^9, the cfg3s
-horizon) and K in {1, 2, 3}, N_p = W, and appends each JSON line to out.jsonl."""
+Runs bench.py under torchrun for N_t in {2^11, 2^12, 2^13, 2^14} (N_C = 2^9, the cfg3s
+horizon: N_t / N_C = 4, 8, 16, 32 with cfg5's step sizes) and K in {1, 2, 3}, N_p = W,
+and appends each JSON line to out.jsonl."""
 import json
 import os
 import subprocess
@@ -12,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 W, out = int(sys.argv[1]), sys.argv[2]
 extra = sys.argv[3:]
 port = 29600
-for Nt in (2 ** 12, 2 ** 13, 2 ** 14):
+for Nt in (2 ** 11, 2 ** 12, 2 ** 13, 2 ** 14):
     for K in (1, 2, 3):
         if K > W:
             continue
@@ -32,4 +33,5 @@ for Nt in (2 ** 12, 2 ** 13, 2 ** 14):
         sp = d["speedup"]
         print(f"Nt={Nt} K={K}: ms={d['ms_per_step']:.0f} S={sp['S_measured']:.3f} "
               f"bound={sp['S_bound_eq_speedup_P229']:.3f} frac={sp['frac_of_bound']:.3f} "
-              f"tc/tf={sp['tau_c_over_tau_f']:.3f} d={sp['defects']}", flush=True)
+              f"tc/tf={sp['tau_c_over_tau_f']:.3f} d={sp['defects']} "
+              f"parity_ok={d.get('parity', {}).get('ok')}", flush=True)
