@@ -88,6 +88,51 @@ __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// ---- Tensor memory (TMEM) as a warp-to-warp staging buffer (FusedCfgP::TM = 1).
+// 128 lanes x 512 columns of 32 bits per SM; warp w reaches lanes 32 (w % 4) .. +31 with
+// tcgen05.ld / tcgen05.st (thread i <-> lane 32 (w % 4) + i), a datapath separate from
+// shared memory.  A stage-A warp and the stage-B warp of the same lane quadrant hand
+// per-point values over through it instead of through the shared intermediate ring.
+__device__ __forceinline__ void tm_alloc(uint32_t *dst_smem, uint32_t ncols) {  // one warp
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tm_dealloc(uint32_t taddr, uint32_t ncols) {  // the allocating warp
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tm_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tm_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// 8 columns (two rows of a lane's two x points) from / to this thread's lane
+__device__ __forceinline__ void tm_st8(uint32_t taddr, double2 a, double2 b) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "r"(__double2loint(a.x)), "r"(__double2hiint(a.x)), "r"(__double2loint(a.y)),
+                 "r"(__double2hiint(a.y)), "r"(__double2loint(b.x)), "r"(__double2hiint(b.x)),
+                 "r"(__double2loint(b.y)), "r"(__double2hiint(b.y))
+                 : "memory");
+}
+struct TmRaw8 { uint32_t r[8]; };
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, TmRaw8 &v) {  // tm_wait_ld() before use
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v.r[0]), "=r"(v.r[1]), "=r"(v.r[2]), "=r"(v.r[3]), "=r"(v.r[4]), "=r"(v.r[5]),
+                   "=r"(v.r[6]), "=r"(v.r[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+__device__ __forceinline__ double2 tm_row(const TmRaw8 &v, int r) {  // row r of the two
+    double2 d;
+    d.x = __hiloint2double(int(v.r[4 * r + 1]), int(v.r[4 * r + 0]));
+    d.y = __hiloint2double(int(v.r[4 * r + 3]), int(v.r[4 * r + 2]));
+    return d;
+}
+
 // folded 13-point operator, C3 (same order as stencil_kernel)
 struct Weights {
     double wm1[3], wp1[3], wm2[3], wp2[3], w0;
@@ -167,7 +212,7 @@ __device__ __forceinline__ double2 apply_pair(const Weights &W, double2 L, doubl
 // compute warps finish the current one (no per-item pipeline fill).  Aux planes
 // (K_B) share the slot index of the input element they ride with.
 template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_, int PW_ = 1, int FILL_ = 0,
-          int UIN_ = 0, int DEPTHA_ = DEPTH_>
+          int UIN_ = 0, int DEPTHA_ = DEPTH_, int TM_ = 0>
 struct FusedCfgP {
     static constexpr bool COMB = false;  // comb.cuh configs: stage B in the stage-A lanes
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = 1, XP = 2,
@@ -187,6 +232,17 @@ struct FusedCfgP {
     static constexpr int A_ITEMS = (EW / 2) * GA, B_ITEMS = (TXO / 2) * GB;
     static constexpr int WA = (A_ITEMS + 31) / 32, WB = (B_ITEMS + 31) / 32;
     static constexpr int NTA = 32 * WA, NTB = 32 * WB, NTP = 32 * PW, NT = NTA + NTB + NTP;
+    // TM: the per-point values stage B needs from stage A (its intermediate-plane z column,
+    // t0 and, in K_A, u) go through tensor memory.  Thread layout [stage-A tile lanes |
+    // stage B | stage-A ring lanes | producers], so that stage-A tile lane i and stage-B
+    // lane i sit in warps of the same TMEM lane quadrant.
+    static constexpr int TM = TM_;
+    static constexpr int NTC = (TXO / 2) * (TYO / RPTA_);  // stage-A lanes on the tile
+    static constexpr int B_BASE = TM ? NTC : NTA;           // first stage-B thread
+    static constexpr int R_LANES = A_ITEMS - NTC;           // stage-A lanes on the halo ring
+    static constexpr int TM_PLANE = 24;                     // TMEM columns per plane
+    static constexpr int TM_COLS = TM_PLANE * ZD_ <= 32 ? 32 : TM_PLANE * ZD_ <= 64 ? 64 :
+                                   TM_PLANE * ZD_ <= 128 ? 128 : TM_PLANE * ZD_ <= 256 ? 256 : 512;
     // register cap: the whole register file for one CTA of NT threads (multiple of 8),
     // or PRK_FUSED_MAXR when the build defines it (tuning)
 #ifdef PRK_FUSED_MAXR
@@ -202,11 +258,13 @@ struct FusedCfgP {
     static_assert(TYO % RPT == 0 && EH % RPTA == 0, "rows must split into row groups");
     static_assert(Y_ELEMS % 16 == 0 && Z_ELEMS % 16 == 0, "slots must stay 128-byte aligned");
     static_assert(DEPTH >= 5 && ZD >= 3, "rings too shallow");
+    static_assert(!TM_ || (RPTA_ == RPTB_ && NTC % 128 == 0 && NTC == 32 * WB && !UIN_),
+                  "TMEM hand-off: stage-A tile lanes map 1:1 onto stage-B lanes, four warps each");
     // input ring depth per kernel: K_A has shared memory to spare (no aux ring)
     template <int KB> static constexpr int DEPTH_K = KB == K_A ? DEPTHA_ : DEPTH;
     template <int KB> static constexpr int NTV = (KB == K_A && !UIN) ? 2 : 1;
     template <int KB> static constexpr int IN_CONSUMERS = (KB == K_A && UIN) ? NTA + NTB : NTA;
-    template <int KB> static constexpr int ZS_ELEMS = Z_ELEMS + NTV<KB> * T_ELEMS;
+    template <int KB> static constexpr int ZS_ELEMS = Z_ELEMS + (TM ? 0 : NTV<KB> * T_ELEMS);
     template <int KB> static constexpr size_t smem_bytes() {
         return sizeof(double) * (size_t(DEPTH_K<KB>) * Y_ELEMS + (KB == K_B ? size_t(AD) * AUX_ELEMS : 0) +
                                  size_t(ZD) * ZS_ELEMS<KB>);
@@ -217,6 +275,8 @@ using FusedP4 = FusedCfgP<16, 9, 4, 2, 2, 2, 2>;  // 32x16 tile, TMA tensor fill
 // recomputes 27 % instead of 41 %, and each lane reads 2 instead of 2.5 shared values per point
 using FusedT32 = FusedCfgP<32, 7, 4, 4, 4, 2, 2, 0, 7>;
 using FusedT32B = FusedCfgP<32, 5, 3, 4, 4, 2, 2, 0, 5>;  // K_B at 32x32: shallower rings to fit
+// 32x16 tile with the stage A -> stage B per-point hand-off through tensor memory
+using FusedTM = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 1>;
 #ifdef PRK_VARIANTS  // tuning history (profiles/r01_kernel_bench_variants.txt)
 using FusedP0 = FusedCfgP<16, 7, 4, 2, 2, 1>;   // one producer warp
 using FusedP1 = FusedCfgP<16, 9, 4, 2, 2, 1>;
@@ -406,14 +466,20 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
 template <int KB, class C>
 __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int items,
                                           uint64_t *full, uint64_t *empty, uint64_t *in_full,
-                                          uint64_t *in_empty) {
+                                          uint64_t *in_empty, uint32_t tmem) {
     constexpr int RPT = C::RPTA, DEPTH = C::template DEPTH_K<KB>, EW = C::EWS, IW = C::IWS, TXO = C::TXO,
                   ZD = C::ZD;
     constexpr int ZS = C::template ZS_ELEMS<KB>;
     double *yring = sm;
     double *aring = yring + size_t(DEPTH) * C::Y_ELEMS;
     double *zring = aring + (KB == K_B ? size_t(C::AD) * C::AUX_ELEMS : 0);
-    const int t = threadIdx.x;
+    // stage-A lane index: TM puts the tile lanes first (threads 0 .. NTC-1) and the ring
+    // lanes after the stage-B threads
+    const int t = (!C::TM || threadIdx.x < C::NTC) ? int(threadIdx.x)
+                                                    : C::NTC + int(threadIdx.x) - (C::B_BASE + C::NTB);
+    const bool tile_lane = C::TM && t < C::NTC;  // writes its per-point values to TMEM
+    // TMEM address of this warp's lane quadrant
+    const uint32_t tq_addr = tmem + (uint32_t(32 * ((threadIdx.x >> 5) & 3)) << 16);
 
     const long long row = (*a.nu_pos + a.j_local) * 4;
     Weights W;
@@ -421,7 +487,19 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
     const double dt = a.dt;
 
     const bool valid = t < C::A_ITEMS;
-    const int l = valid ? t % (C::EW / 2) : 0, g = valid ? t / (C::EW / 2) : 0;
+    int l = valid ? t % (C::EW / 2) : 0, g = valid ? t / (C::EW / 2) : 0;
+    if constexpr (C::TM) {  // tile lanes as stage B's lanes, then the ring (comb.cuh's map)
+        if (t < C::NTC) {
+            l = t % (TXO / 2) + 1;
+            g = t / (TXO / 2) + 1;
+        } else {
+            const int u = t - C::NTC, top = C::EW / 2;
+            if (!valid) { l = 0; g = 0; }
+            else if (u < top) { l = u; g = 0; }
+            else if (u < 2 * top) { l = u - top; g = C::EH / RPT - 1; }
+            else { const int v = u - 2 * top; l = (v & 1) ? top - 1 : 0; g = 1 + (v >> 1); }
+        }
+    }
     const int r0 = g * RPT;
     const int sY = (r0 + 2) * IW + 2 * l + 2;
     const int sZ = r0 * EW + 2 * l;
@@ -464,7 +542,7 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
             // K_B: u on the ring is in shared memory already; load it before the
             // stencil so its latency hides under the FMAs
             const double *au = aring + size_t(p4.slot) * C::AUX_ELEMS;  // aux j
-            const bool outp = j >= 2 && j < w.nz + 2;
+            [[maybe_unused]] const bool outp = j >= 2 && j < w.nz + 2;
             double2 ubv[KB == K_B ? RPT : 1];
             if constexpr (KB == K_B) {
 #pragma unroll
@@ -489,7 +567,50 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
             }
             if (zpos.round > 0) mbar_wait(&empty[zpos.slot], (zpos.round - 1) & 1);
             double *zs = zring + size_t(zpos.slot) * ZS;
-            if (valid) {
+            if constexpr (C::TM) {
+                if (tile_lane) {  // intermediate centre, t0 (and u) of this plane -> TMEM
+                    tm_fence_after();
+                    double2 zz[RPT], t0v[RPT];
+#pragma unroll
+                    for (int r = 0; r < RPT; ++r) {
+                        const double2 yc = q[r][(P + 2) % 5];
+                        if (KB == K_A) {
+                            zz[r].x = yc.x + (dt / 2.0) * k[r].x;
+                            zz[r].y = yc.y + (dt / 2.0) * k[r].y;
+                            t0v[r].x = yc.x + (dt / 6.0) * k[r].x;
+                            t0v[r].y = yc.y + (dt / 6.0) * k[r].y;
+                        } else {
+                            const double2 ub = ubv[KB == K_B ? r : 0], ac = acv[KB == K_B ? r : 0];
+                            zz[r].x = ub.x + dt * k[r].x;
+                            zz[r].y = ub.y + dt * k[r].y;
+                            t0v[r].x = ac.x + (dt / 3.0) * k[r].x;
+                            t0v[r].y = ac.y + (dt / 3.0) * k[r].y;
+                        }
+                        sts2(zs + sZ + r * EW, zz[r]);  // x/y neighbours for stage B
+                    }
+                    const uint32_t col = tq_addr + uint32_t(zpos.slot * C::TM_PLANE);
+                    tm_st8(col, zz[0], zz[1]);
+                    tm_st8(col + 8, t0v[0], t0v[1]);
+                    if (KB == K_A) tm_st8(col + 16, q[0][(P + 2) % 5], q[1][(P + 2) % 5]);
+                    tm_wait_st();
+                    tm_fence_before();
+                } else if (valid) {
+#pragma unroll
+                    for (int r = 0; r < RPT; ++r) {
+                        double2 z;
+                        if (KB == K_A) {
+                            const double2 yc = q[r][(P + 2) % 5];
+                            z.x = yc.x + (dt / 2.0) * k[r].x;
+                            z.y = yc.y + (dt / 2.0) * k[r].y;
+                        } else {
+                            const double2 ub = ubv[KB == K_B ? r : 0];
+                            z.x = ub.x + dt * k[r].x;
+                            z.y = ub.y + dt * k[r].y;
+                        }
+                        sts2(zs + sZ + r * EW, z);
+                    }
+                }
+            } else if (valid) {
 #pragma unroll
                 for (int r = 0; r < RPT; ++r) {
                     const double2 yc = q[r][(P + 2) % 5];
@@ -538,15 +659,17 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
 
 template <int KB, class C>
 __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int items,
-                                          uint64_t *full, uint64_t *empty, uint64_t *in_empty) {
+                                          uint64_t *full, uint64_t *empty, uint64_t *in_empty,
+                                          uint32_t tmem) {
     constexpr bool UIN = KB == K_A && C::UIN;
     constexpr int RPT = C::RPT, EW = C::EWS, TXO = C::TXO, ZD = C::ZD, DEPTH = C::template DEPTH_K<KB>;
     constexpr int ZS = C::template ZS_ELEMS<KB>;
     double *zring = sm + size_t(DEPTH) * C::Y_ELEMS + (KB == K_B ? size_t(C::AD) * C::AUX_ELEMS : 0);
     const int n = a.n;
     const size_t nn = size_t(n) * n;
-    const int tb = threadIdx.x - C::NTA;
+    const int tb = threadIdx.x - C::B_BASE;
     const bool valid = tb < C::B_ITEMS;
+    const uint32_t tq_addr = tmem + (uint32_t(32 * ((threadIdx.x >> 5) & 3)) << 16);
     const int m = valid ? tb % (TXO / 2) : 0, g = valid ? tb / (TXO / 2) : 0;
     const int r0 = g * RPT;
     const int sZ = (r0 + 2) * EW + 2 * m + 2;
@@ -575,9 +698,18 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
         rotating_loop(NJ, [&](auto ph, int j) {
             constexpr int P = decltype(ph)::value;
             mbar_wait(&full[zq_pos.slot], zq_pos.round & 1);
-            const double *zq = zring + size_t(zq_pos.slot) * ZS + sZ;
+            if constexpr (C::TM) {
+                tm_fence_after();
+                TmRaw8 tz;
+                tm_ld8(tq_addr + uint32_t(zq_pos.slot * C::TM_PLANE), tz);  // own centre, plane j
+                tm_wait_ld();
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = lds2(zq + r * EW);
+                for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = tm_row(tz, r);
+            } else {
+                const double *zq = zring + size_t(zq_pos.slot) * ZS + sZ;
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = lds2(zq + r * EW);
+            }
             if (j >= 4 && valid) {
                 const double *zs = zring + size_t(zc_pos.slot) * ZS;
                 const double *zc = zs + sZ;
@@ -585,24 +717,36 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
 #pragma unroll
                 for (int r = 0; r < RPT + 4; ++r)
                     col[r] = (r >= 2 && r < RPT + 2) ? q[r - 2][(P + 2) % 5] : lds2(zc + (r - 2) * EW);
+                double2 kBs[RPT];
+#pragma unroll
+                for (int r = 0; r < RPT; ++r)
+                    kBs[r] = apply_pair<P>(W, lds2(zc + r * EW - 2), lds2(zc + r * EW + 2), col[r], col[r + 1],
+                                           col[r + 3], col[r + 4], q[r]);
+                TmRaw8 tt0, tt1;  // TM: t0 and u of the output point (plane j-2)
+                if constexpr (C::TM) {
+                    const uint32_t cc = tq_addr + uint32_t(zc_pos.slot * C::TM_PLANE);
+                    tm_ld8(cc + 8, tt0);
+                    if (KB == K_A) tm_ld8(cc + 16, tt1);
+                    tm_wait_ld();
+                }
 #pragma unroll
                 for (int r = 0; r < RPT; ++r) {
-                    const double2 kB = apply_pair<P>(W, lds2(zc + r * EW - 2), lds2(zc + r * EW + 2),
-                                                     col[r], col[r + 1], col[r + 3], col[r + 4], q[r]);
+                    const double2 kB = kBs[r];
                     const size_t gofs = size_t(r) * n;
                     if (KB == K_A) {
-                        const double2 t0 = lds2(zs + C::Z_ELEMS + sT + r * TXO);
+                        const double2 t0 = C::TM ? tm_row(tt0, r) : lds2(zs + C::Z_ELEMS + sT + r * TXO);
                         // u at the output point: input element j (plane z_begin + j - 4)
                         const double2 t1 =
-                            UIN ? lds2(yring + size_t(in_pos.slot) * C::Y_ELEMS + sU + r * C::IWS)
-                                : lds2(zs + C::Z_ELEMS + C::T_ELEMS + sT + r * TXO);
+                            C::TM ? tm_row(tt1, r)
+                            : UIN ? lds2(yring + size_t(in_pos.slot) * C::Y_ELEMS + sU + r * C::IWS)
+                                  : lds2(zs + C::Z_ELEMS + C::T_ELEMS + sT + r * TXO);
                         double2 v0, v1;
                         v0.x = t0.x + (dt / 3.0) * kB.x;  v0.y = t0.y + (dt / 3.0) * kB.y;
                         v1.x = t1.x + (dt / 2.0) * kB.x;  v1.y = t1.y + (dt / 2.0) * kB.y;
                         *reinterpret_cast<double2 *>(o0 + gofs) = v0;
                         *reinterpret_cast<double2 *>(o1 + gofs) = v1;
                     } else {
-                        const double2 t0 = lds2(zs + C::Z_ELEMS + sT + r * TXO);
+                        const double2 t0 = C::TM ? tm_row(tt0, r) : lds2(zs + C::Z_ELEMS + sT + r * TXO);
                         double2 v0;
                         v0.x = t0.x + (dt / 6.0) * kB.x;  v0.y = t0.y + (dt / 6.0) * kB.y;
                         *reinterpret_cast<double2 *>(o0 + gofs) = v0;
@@ -614,6 +758,7 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
                 if (KB == K_A) o1 += nn;
             }
             if (j >= 2) {
+                if constexpr (C::TM) tm_fence_before();
                 mbar_arrive(&empty[zc_pos.slot]);
                 zc_pos.step(ZD);
             }
@@ -818,13 +963,35 @@ fused_persist_kernel(const StencilArgs a, const __grid_constant__ TmaMaps tm) {
         }
         fence_mbar_init();
     }
-    __syncthreads();
-    if (threadIdx.x < C::NTA)
-        stage_a_p<KB, C>(a, sm, items, full, empty, in_full, in_empty);
-    else if (threadIdx.x < C::NTA + C::NTB)
-        stage_b_p<KB, C>(a, sm, items, full, empty, in_empty);
+    uint32_t tmem = 0;
+    if constexpr (C::TM) {  // warp 0 allocates the TMEM hand-off ring
+        __shared__ uint32_t tmem_base;
+        if (threadIdx.x < 32) tm_alloc(&tmem_base, C::TM_COLS);
+        tm_fence_before();
+        __syncthreads();
+        tm_fence_after();
+        tmem = tmem_base;
+    } else {
+        __syncthreads();
+    }
+    const int tid = threadIdx.x;
+    const bool is_a = C::TM ? (tid < C::NTC || (tid >= C::B_BASE + C::NTB && tid < C::NTA + C::NTB))
+                            : tid < C::NTA;
+    const bool is_b = tid >= C::B_BASE && tid < C::B_BASE + C::NTB;
+    if (is_a)
+        stage_a_p<KB, C>(a, sm, items, full, empty, in_full, in_empty, tmem);
+    else if (is_b)
+        stage_b_p<KB, C>(a, sm, items, full, empty, in_empty, tmem);
     else
         producer_p<KB, C>(a, &tm, sm, items, in_full, in_empty);
+    if constexpr (C::TM) {
+        tm_fence_before();
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            tm_fence_after();
+            tm_dealloc(tmem, C::TM_COLS);
+        }
+    }
 }
 
 }  // namespace prk

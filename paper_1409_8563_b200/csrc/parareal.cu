@@ -389,7 +389,8 @@ static void launch_coarse_persist(pr_grid *g, const StencilArgs &a0, cudaStream_
 // (K_A: stages 1+2, K_B: stages 3+4; they are independent launches over the whole
 // grid, so their tilings may differ).  X(id, config of K_A, config of K_B)
 #define PRK_FVARIANTS(X) \
-    X(14, FusedP4, FusedP4) X(20, FusedT32, FusedP4) X(21, FusedT32, FusedT32B) X(22, Comb16, Comb16)
+    X(14, FusedP4, FusedP4) X(20, FusedT32, FusedP4) X(21, FusedT32, FusedT32B) X(22, Comb16, Comb16) \
+    X(23, FusedTM, FusedTM)
 #ifdef PRK_VARIANTS
 #define PRK_FVARIANTS_OLD(X)                                                                    \
     X(10, FusedP0, FusedP0) X(11, FusedP1, FusedP1) X(12, FusedP2, FusedP2) X(13, FusedP3, FusedP3) \
@@ -1222,6 +1223,20 @@ pr_status pr_comm_init(pr_grid *g, int32_t world, int32_t rank, const void *id) 
         return fail(PR_ENCCL, "rank %d: ncclCommInitRank: %s", rank, ncclGetErrorString(r));
     }
     if (!g->comm_stream) CK(cudaStreamCreateWithFlags(&g->comm_stream, cudaStreamNonBlocking));
+    // Connect the pipeline's links now, while every rank is inside this collective call:
+    // NCCL sets up a point-to-point connection at its first use, and that handshake
+    // blocks the host until the peer joins, so a predecessor that never reaches
+    // pr_parareal would hang the successor inside ncclRecv instead of failing it.
+    if (world > 1) {
+        if (!g->d_red) CK(cudaMalloc(&g->d_red, 8 * sizeof(unsigned long long)));
+        ncclGroupStart();
+        if (rank + 1 < world) ncclSend(g->d_red, 1, ncclUint64, rank + 1, g->comm, g->comm_stream);
+        if (rank > 0) ncclRecv(g->d_red + 1, 1, ncclUint64, rank - 1, g->comm, g->comm_stream);
+        r = ncclGroupEnd();
+        if (r != ncclSuccess)
+            return fail(PR_ENCCL, "rank %d: connecting the pipeline links: %s", rank, ncclGetErrorString(r));
+        CK(cudaStreamSynchronize(g->comm_stream));
+    }
     g->lgroup.reset();  // a communicator replaces an in-process rank group
     g->world = world;
     g->rank = rank;
