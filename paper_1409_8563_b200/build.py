@@ -36,7 +36,7 @@ def nvcc_cmd(out: str, debug: bool = False) -> list[str]:
     inc, lib = nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     return [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
-            "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared", "-Xptxas", "-v",
+            "-std=c++17", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-shared", "-Xptxas", "-v",
             *(["-DPRK_DEBUG"] if debug else []),
             "-I", os.path.join(ROOT, "include"), "-I", inc,
             *SRCS, "-o", out, "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}"]

@@ -136,15 +136,17 @@ __device__ __forceinline__ double2 tm_row(const TmRaw8 &v, int r) {  // row r of
 // folded 13-point operator, C3 (same order as stencil_kernel)
 struct Weights {
     double wm1[3], wp1[3], wm2[3], wp2[3], w0;
-    __device__ __forceinline__ void set(double nu, double inv_dx, const double *c) {
-        const double al = nu * inv_dx * inv_dx / 12.0;
-        w0 = -90.0 * al;
+    __device__ __forceinline__ void load(const double *w) {  // fine_weights13 layout
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            const double be = c[d] * inv_dx / 12.0;
-            wp2[d] = -al + be; wp1[d] = 16.0 * al - 8.0 * be;
-            wm1[d] = 16.0 * al + 8.0 * be; wm2[d] = -al - be;
+            wm1[d] = w[d]; wp1[d] = w[3 + d]; wm2[d] = w[6 + d]; wp2[d] = w[9 + d];
         }
+        w0 = w[12];
+    }
+    __device__ __forceinline__ void set(double nu, double inv_dx, const double *c) {
+        double w[13];
+        fine_weights13(nu, inv_dx, c, w);
+        load(w);
     }
 };
 
@@ -215,6 +217,7 @@ template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_, int PW_ = 1, int 
           int UIN_ = 0, int DEPTHA_ = DEPTH_, int TM_ = 0>
 struct FusedCfgP {
     static constexpr bool COMB = false;  // comb.cuh configs: stage B in the stage-A lanes
+    static constexpr bool WP = false;    // weights from the nu table (graph replays)
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = 1, XP = 2,
                          PROD = 1, PW = PW_;  // PW producer warps
     // FILL 0: every plane by 16-byte cp.async; 2: planes of tiles away from the
@@ -277,6 +280,9 @@ using FusedT32 = FusedCfgP<32, 7, 4, 4, 4, 2, 2, 0, 7>;
 using FusedT32B = FusedCfgP<32, 5, 3, 4, 4, 2, 2, 0, 5>;  // K_B at 32x32: shallower rings to fit
 // 32x16 tile with the stage A -> stage B per-point hand-off through tensor memory
 using FusedTM = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 1>;
+// the same kernel with the two stages' weights passed as launch parameters (direct launches):
+// they sit in uniform registers / the constant bank instead of 26 registers per thread
+template <class C> struct WithWP : C { static constexpr bool WP = true; };
 #ifdef PRK_VARIANTS  // tuning history (profiles/r01_kernel_bench_variants.txt)
 using FusedP0 = FusedCfgP<16, 7, 4, 2, 2, 1>;   // one producer warp
 using FusedP1 = FusedCfgP<16, 9, 4, 2, 2, 1>;
@@ -481,9 +487,13 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
     // TMEM address of this warp's lane quadrant
     const uint32_t tq_addr = tmem + (uint32_t(32 * ((threadIdx.x >> 5) & 3)) << 16);
 
-    const long long row = (*a.nu_pos + a.j_local) * 4;
     Weights W;
-    W.set(a.nu_tab[row + (KB == K_A ? 0 : 2)], a.inv_dx, a.c);
+    if constexpr (C::WP) {
+        W.load(a.wA);
+    } else {
+        const long long row = (*a.nu_pos + a.j_local) * 4;
+        W.set(a.nu_tab[row + (KB == K_A ? 0 : 2)], a.inv_dx, a.c);
+    }
     const double dt = a.dt;
 
     const bool valid = t < C::A_ITEMS;
@@ -679,9 +689,13 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
     const double *yring = sm;
     const int sU = (r0 + C::HY) * C::IWS + 2 * m + C::HX;  // tile point in an input slot
 
-    const long long row = (*a.nu_pos + a.j_local) * 4;
     Weights W;
-    W.set(a.nu_tab[row + (KB == K_A ? 1 : 3)], a.inv_dx, a.c);
+    if constexpr (C::WP) {
+        W.load(a.wB);
+    } else {
+        const long long row = (*a.nu_pos + a.j_local) * 4;
+        W.set(a.nu_tab[row + (KB == K_A ? 1 : 3)], a.inv_dx, a.c);
+    }
     const double dt = a.dt;
 
     RingPos zq_pos;  // Z plane j of the current item

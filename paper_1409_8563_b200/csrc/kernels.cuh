@@ -78,6 +78,35 @@ template <int KIND, class C> struct Layout {
     static constexpr int P_CHUNKS = NP * C::TY * (TX / 2);
 };
 
+// Folded 13-point RHS weights of the fine operator (C3):
+//   L(y) = w0 y + sum_a [wm1_a y_{-a} + wp1_a y_{+a} + wm2_a y_{-2a} + wp2_a y_{+2a}]
+// with al = nu/(12 dx^2), be_a = c_a/(12 dx).  Layout w[13] = {wm1[3], wp1[3], wm2[3],
+// wp2[3], w0}.  Every product and sum is rounded separately (no FMA contraction) so the
+// host (weights passed as kernel parameters) and the device (weights from the nu table)
+// produce the same bits.
+__host__ __device__ __forceinline__ void fine_weights13(double nu, double inv_dx, const double *c, double *w) {
+#ifdef __CUDA_ARCH__
+    auto mul = [](double x, double y) { return __dmul_rn(x, y); };
+    auto add = [](double x, double y) { return __dadd_rn(x, y); };
+    auto sub = [](double x, double y) { return __dsub_rn(x, y); };
+    auto div = [](double x, double y) { return __ddiv_rn(x, y); };
+#else
+    auto mul = [](double x, double y) { return x * y; };
+    auto add = [](double x, double y) { return x + y; };
+    auto sub = [](double x, double y) { return x - y; };
+    auto div = [](double x, double y) { return x / y; };
+#endif
+    const double al = div(mul(mul(nu, inv_dx), inv_dx), 12.0);
+    w[12] = mul(-90.0, al);
+    for (int d = 0; d < 3; ++d) {
+        const double be = div(mul(c[d], inv_dx), 12.0);
+        w[6 + d] = sub(-al, be);                          // wm2
+        w[9 + d] = add(-al, be);                          // wp2
+        w[3 + d] = sub(mul(16.0, al), mul(8.0, be));      // wp1
+        w[d] = add(mul(16.0, al), mul(8.0, be));          // wm1
+    }
+}
+
 struct StencilArgs {
     const double *y;    // stencil input (read with halo)
     const double *p0;   // pointwise input 0 (u for S2/S3, acc for S4)
@@ -92,6 +121,8 @@ struct StencilArgs {
     double inv_dx;      // 1/dx
     double c[3];        // advection velocity
     double dt;          // step size (delta t or Delta t)
+    double wA[13], wB[13];  // fine weights of the launch's two stages when passed as
+                            // parameters (direct launches, fine_weights13 layout)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -243,14 +274,13 @@ stencil_kernel(const StencilArgs a) {
     } else {
         // rhs = nu Lap4 u - c . Grad4 u  with weights (-1,16,-30,16,-1)/12dx^2
         // and (-1,8,0,-8,1)/12dx on offsets (+2,+1,0,-1,-2)   (C3)
-        const double al = nu * a.inv_dx * a.inv_dx / 12.0;
-        w0 = -90.0 * al;
+        double w[13];
+        fine_weights13(nu, a.inv_dx, a.c, w);
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            const double be = a.c[d] * a.inv_dx / 12.0;
-            wp2[d] = -al + be; wp1[d] = 16.0 * al - 8.0 * be;
-            wm1[d] = 16.0 * al + 8.0 * be; wm2[d] = -al - be;
+            wm1[d] = w[d]; wp1[d] = w[3 + d]; wm2[d] = w[6 + d]; wp2[d] = w[9 + d];
         }
+        w0 = w[12];
     }
     const double dt = a.dt;
     const bool col_ok = tx < w;

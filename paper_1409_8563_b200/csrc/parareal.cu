@@ -28,6 +28,7 @@
 #include "kernels.cuh"
 #include "fused.cuh"
 #include "comb.cuh"
+#include "onestep.cuh"
 
 using namespace prk;
 
@@ -117,6 +118,8 @@ struct LocalGroup {
 struct pr_grid {
     int dev = 0;
     int variant = 0;                    // stencil tile variant (PR_TILE env, tuning)
+    bool f1 = false;                    // F as ONE kernel per RK4 step (variant 24, NEXT-1)
+    bool wparam = false;                // fused F launched directly, weights as parameters
     bool f2 = false;                    // fused two-kernel RK4 step (tile-aligned n)
     int fvariant = 14;                  // fused tile variant (PR_FTILE env 10..19, tuning)
     bool c2 = false;                    // persistent TMA-fed G kernel (n % 32 == 0; PR_C2=0 disables)
@@ -296,7 +299,8 @@ static pr_status setup_kind(pr_grid *g) {
 // stage-A lanes (comb.cuh)
 template <int KB, class C>
 static constexpr auto fused_kernel_of() {
-    if constexpr (C::COMB) return &fused_comb_kernel<KB, C>;
+    if constexpr (std::is_same_v<C, OneCfg>) return &onestep_kernel<KB, C>;
+    else if constexpr (C::COMB) return &fused_comb_kernel<KB, C>;
     else return &fused_persist_kernel<KB, C>;
 }
 
@@ -323,7 +327,7 @@ static pr_status setup_fused_persist(pr_grid *g) {
     c.tiles_x = n / C::TXO;
     c.tiles_y = n / C::TYO;
     const int slots = g->sms * occ;
-    const int ch = pick_chunks(n, c.tiles_x * c.tiles_y, slots, 4);
+    const int ch = pick_chunks(n, c.tiles_x * c.tiles_y, slots, std::is_same_v<C, OneCfg> ? 8 : 4);
     c.cz = (n + ch - 1) / ch;
     c.chunks_z = (n + c.cz - 1) / c.cz;
     const int items = c.tiles_x * c.tiles_y * c.chunks_z;
@@ -390,7 +394,7 @@ static void launch_coarse_persist(pr_grid *g, const StencilArgs &a0, cudaStream_
 // grid, so their tilings may differ).  X(id, config of K_A, config of K_B)
 #define PRK_FVARIANTS(X) \
     X(14, FusedP4, FusedP4) X(20, FusedT32, FusedP4) X(21, FusedT32, FusedT32B) X(22, Comb16, Comb16) \
-    X(23, FusedTM, FusedTM)
+    X(23, FusedTM, FusedTM) X(24, OneCfg, OneCfg)
 #ifdef PRK_VARIANTS
 #define PRK_FVARIANTS_OLD(X)                                                                    \
     X(10, FusedP0, FusedP0) X(11, FusedP1, FusedP1) X(12, FusedP2, FusedP2) X(13, FusedP3, FusedP3) \
@@ -412,8 +416,27 @@ static void fused_tiles(int v, int *tya, int *tyb) {
     }
 }
 
+// variants that also exist with the weights as launch parameters (WithWP)
+#define PRK_FVARIANTS_WP(X) X(14, FusedP4, FusedP4) X(23, FusedTM, FusedTM)
+static bool fused_has_wp(int v) {
+    switch (v) {
+#define X(id, A, B) case id: return true;
+        PRK_FVARIANTS_WP(X)
+#undef X
+    default: return false;
+    }
+}
+
 template <int KB>
 static pr_status setup_fused(pr_grid *g) {
+    if (g->wparam) {
+        switch (g->fvariant) {
+#define X(id, A, B) case id: return setup_fused_persist<KB, WithWP<PickCfg<KB, A, B>>>(g);
+            PRK_FVARIANTS_WP(X)
+#undef X
+        default: break;
+        }
+    }
     switch (g->fvariant) {
 #define X(id, A, B) case id: return setup_fused_persist<KB, PickCfg<KB, A, B>>(g);
         PRK_FVARIANTS(X) PRK_FVARIANTS_OLD(X)
@@ -449,11 +472,22 @@ static void launch_fused(pr_grid *g, const StencilArgs &a0, cudaStream_t st) {
     a.tiles_y = c.tiles_y;
     a.cz = c.cz;
     a.chunks_z = c.chunks_z;
-    switch (g->fvariant) {
-#define X(id, A, B) case id: launch_persist<KB, PickCfg<KB, A, B>>(g, a, c, st); break;
-        PRK_FVARIANTS(X) PRK_FVARIANTS_OLD(X)
+    bool done = false;
+    if (g->wparam) {
+        switch (g->fvariant) {
+#define X(id, A, B) case id: launch_persist<KB, WithWP<PickCfg<KB, A, B>>>(g, a, c, st); done = true; break;
+            PRK_FVARIANTS_WP(X)
 #undef X
-    default: break;
+        default: break;
+        }
+    }
+    if (!done) {
+        switch (g->fvariant) {
+#define X(id, A, B) case id: launch_persist<KB, PickCfg<KB, A, B>>(g, a, c, st); break;
+            PRK_FVARIANTS(X) PRK_FVARIANTS_OLD(X)
+#undef X
+        default: break;
+        }
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -512,20 +546,45 @@ static void enqueue_fine_step(pr_grid *g, const double *u_src, double *u_dst, in
     launch_stencil<K_S4>(g, a, st);
 }
 
+static inline double nu_of(const pr_problem &p, double t);
+
+// nu of RK4 stage s (0..3) of global fine step j: the expressions of the device table
+// (ensure_table; readings C1, C6)
+static double nu_stage(const pr_grid *g, int64_t j, int s, double dt) {
+    const pr_problem &p = g->prob;
+    if (p.nu_mode == PR_NU_STEP_START || s == 0) return nu_of(p, double(j) * dt);
+    if (s == 3) return nu_of(p, (double(j) + 1.0) * dt);
+    return nu_of(p, (double(j) + 0.5) * dt);
+}
+
 // One classical RK4 step as two fused kernels (fused.cuh): state u_src ->
-// new state in acc_dst (u_src is only read; Yb lives in g->ya).
+// new state in acc_dst (u_src is only read; Yb lives in g->ya).  jglob: the global
+// step index, used when the weights travel as launch parameters (g->wparam).
 static void enqueue_fine_step2(pr_grid *g, const double *u_src, double *acc_dst, int j_local,
-                               double dt, cudaStream_t st) {
+                               double dt, cudaStream_t st, int64_t jglob = -1) {
     StencilArgs a = base_args(g, K_S1);
     a.nu_tab = g->tab_f.d;
     a.nu_pos = g->d_pos + 0;
     a.j_local = j_local;
     a.dt = dt;
+    if (g->wparam) {  // stage weights of this step on the host (fine_weights13: same bits)
+        fine_weights13(nu_stage(g, jglob, 0, dt), a.inv_dx, a.c, a.wA);
+        fine_weights13(nu_stage(g, jglob, 1, dt), a.inv_dx, a.c, a.wB);
+    }
+    if (g->f1) {  // the whole step in one kernel: u_src -> acc_dst (NEXT-1)
+        a.y = u_src; a.p0 = nullptr; a.p1 = nullptr; a.o0 = acc_dst; a.o1 = nullptr;
+        launch_fused<K_A>(g, a, st);
+        return;
+    }
     // K_A: k1 = L(u), Ya (shared), k2 = L(Ya); acc = u + dt/6 k1 + dt/3 k2; Yb = u + dt/2 k2
     a.y = u_src; a.p0 = nullptr; a.p1 = nullptr; a.o0 = acc_dst; a.o1 = g->ya;
     launch_fused<K_A>(g, a, st);
     // K_B: k3 = L(Yb), Ya' = u + dt k3 (shared), k4 = L(Ya'); u_new = acc + dt/3 k3 + dt/6 k4
     a.y = g->ya; a.p0 = u_src; a.p1 = acc_dst; a.o0 = acc_dst; a.o1 = nullptr;
+    if (g->wparam) {
+        fine_weights13(nu_stage(g, jglob, 2, dt), a.inv_dx, a.c, a.wA);
+        fine_weights13(nu_stage(g, jglob, 3, dt), a.inv_dx, a.c, a.wB);
+    }
     launch_fused<K_B>(g, a, st);
 }
 
@@ -680,7 +739,25 @@ static pr_status get_graph(pr_grid *g, int kind, double *u, double dt, cudaGraph
 // Fused path: the state ping-pongs between u_out and g->acc; the step parity
 // is arranged so the last step lands in u_out.
 static pr_status run_fine2(pr_grid *g, const double *uin, double *uout, int64_t nsteps,
-                           long long base, double dt, cudaStream_t st) {
+                           long long base, double dt, cudaStream_t st, int64_t step0) {
+    if (g->wparam) {  // direct launches, weights as parameters: ping-pong uout <-> acc
+        const double *src = uin;
+        for (int64_t k = 0; k < nsteps; ++k) {
+            // the last step must land in uout: parity of the remaining steps decides
+            double *dst = ((nsteps - k) % 2 == 1) ? uout : g->acc;
+            if (dst == src) dst = (dst == uout) ? g->acc : uout;
+            enqueue_fine_step2(g, src, dst, 0, dt, st, step0 + k);
+            src = dst;
+        }
+        if (src != uout) CK(cudaMemcpyAsync(uout, src, g->bytes, cudaMemcpyDeviceToDevice, st));
+        CKL();
+        if (g->launch_err != PR_OK) {
+            const pr_status e = g->launch_err;
+            g->launch_err = PR_OK;
+            return e;
+        }
+        return PR_OK;
+    }
     int64_t done = 0;
     int jl = 0;
     const double *state = uout;
@@ -703,7 +780,7 @@ static pr_status run_fine2(pr_grid *g, const double *uin, double *uout, int64_t 
         CKS(get_graph(g, 2, uout, dt, &ge));
         while (nsteps - done >= FINE_BATCH) {
             CK(cudaGraphLaunch(ge, st));
-            g_launches.fetch_add(2 * FINE_BATCH + 1, std::memory_order_relaxed);
+            g_launches.fetch_add((g->f1 ? 1 : 2) * FINE_BATCH + 1, std::memory_order_relaxed);
             done += FINE_BATCH;
         }
     }
@@ -737,7 +814,7 @@ static pr_status run_fine(pr_grid *g, const double *uin, double *uout, int64_t s
     if (g->f2) {
         const long long b0 = step0 - g->tab_f.lo;
         CKS(set_pos(g, 0, b0, st));
-        return run_fine2(g, uin, uout, nsteps, b0, dt, st);
+        return run_fine2(g, uin, uout, nsteps, b0, dt, st, step0);
     }
     const long long base = step0 - g->tab_f.lo;
     int64_t done = 0;
@@ -935,10 +1012,16 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
         fused_tiles(g->fvariant, &tya, &tyb);
         if (!tya) return bail(fail(PR_EINVAL, "fused variant %d is not built (PRK_VARIANTS)", g->fvariant));
         g->f2 = (n % FusedP4::TXO == 0) && (n % tya == 0) && (n % tyb == 0) && !(fe && fe[0] == '0');
+        g->f1 = g->f2 && g->fvariant == 24;
+        // large grids: fused kernels launched directly with the weights as parameters
+        // (a launch is ~2 % of a 128^3 step); small grids keep the CUDA-graph batches
+        const char *we = getenv("PR_WPARAM");
+        g->wparam = g->f2 && !g->f1 && fused_has_wp(g->fvariant) &&
+                    (we ? we[0] == '1' : n >= 128);
     }
     if (g->f2) {
         if ((s = setup_fused<K_A>(g)) != PR_OK) return bail(s);
-        if ((s = setup_fused<K_B>(g)) != PR_OK) return bail(s);
+        if (!g->f1 && (s = setup_fused<K_B>(g)) != PR_OK) return bail(s);
     }
     {
         const char *ce = getenv("PR_C2");
@@ -1936,8 +2019,8 @@ pr_status pr_last_monitors(pr_grid *g, double *changes, int32_t cap, int32_t *it
 
 pr_status pr_grid_info(const pr_grid *g, pr_grid_info_t *info) {
     if (!g || !info) return fail(PR_EINVAL, "null argument");
-    info->fine_kernels_per_step = g->f2 ? 2 : 4;
-    info->fine_bytes_per_point = g->f2 ? 56 : 128;
+    info->fine_kernels_per_step = g->f1 ? 1 : g->f2 ? 2 : 4;
+    info->fine_bytes_per_point = g->f1 ? 16 : g->f2 ? 56 : 128;
     info->coarse_bytes_per_point = 16;
     info->sms = g->sms;
     return PR_OK;

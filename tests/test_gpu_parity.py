@@ -234,7 +234,7 @@ def test_fine_paths_agree(n, f2, monkeypatch):
     g.destroy()
 
 
-@pytest.mark.parametrize("variant", [str(v) for v in range(10, 24)])
+@pytest.mark.parametrize("variant", [str(v) for v in range(10, 25)])
 def test_fused_variants_bitwise(variant, monkeypatch):
     """Every persistent fused tile variant (PR_FTILE) gives the four-stage
     path's bits: same folded weights, same operation order per point.  n = 128
@@ -254,6 +254,33 @@ def test_fused_variants_bitwise(variant, monkeypatch):
         outs.append(out)
         g.destroy()
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("variant", ["14", "23"])
+@pytest.mark.parametrize("n", [128, 256])
+def test_weights_as_parameters_bitwise(n, variant, monkeypatch):
+    """Direct launches with the stage weights as kernel parameters (PR_WPARAM=1, the
+    default at n >= 128) give the bits of the CUDA-graph path that reads the weights
+    from the device nu table (PR_WPARAM=0): fine_weights13 rounds every operation
+    separately on host and device.  Odd and even step counts, in place and not."""
+    u0 = dev(random_field(n, 61))
+    outs = []
+    for wp in ("0", "1"):
+        monkeypatch.setenv("PR_FTILE", variant)
+        monkeypatch.setenv("PR_WPARAM", wp)
+        g = pr.Grid(pr.Problem(n, c=PARITY_C))
+        res = []
+        for step0, steps in ((5, 17), (100, 2)):
+            out = torch.empty_like(u0)
+            pr.pr_fine(g, u0, out, step0, steps, 1e-4 * (128 / n) ** 2)
+            res.append(out)
+        u = u0.clone()
+        pr.pr_fine(g, u, u, 7, 3, 1e-4 * (128 / n) ** 2)
+        res.append(u)
+        outs.append(res)
+        g.destroy()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
 
 
 @pytest.mark.parametrize("n", [128, 256])
