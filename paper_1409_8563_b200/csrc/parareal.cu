@@ -1013,11 +1013,12 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
         if (!tya) return bail(fail(PR_EINVAL, "fused variant %d is not built (PRK_VARIANTS)", g->fvariant));
         g->f2 = (n % FusedP4::TXO == 0) && (n % tya == 0) && (n % tyb == 0) && !(fe && fe[0] == '0');
         g->f1 = g->f2 && g->fvariant == 24;
-        // large grids: fused kernels launched directly with the weights as parameters
-        // (a launch is ~2 % of a 128^3 step); small grids keep the CUDA-graph batches
+        // PR_WPARAM=1: fused kernels launched directly with the stage weights as launch
+        // parameters (uniform registers instead of 26 per thread) instead of CUDA-graph
+        // batches reading the nu table.  Measured neutral at 256^3 / 512^3 and 9 % slower
+        // at 128^3 (launch gaps), so the graphs stay the default.
         const char *we = getenv("PR_WPARAM");
-        g->wparam = g->f2 && !g->f1 && fused_has_wp(g->fvariant) &&
-                    (we ? we[0] == '1' : n >= 128);
+        g->wparam = g->f2 && !g->f1 && fused_has_wp(g->fvariant) && we && we[0] == '1';
     }
     if (g->f2) {
         if ((s = setup_fused<K_A>(g)) != PR_OK) return bail(s);

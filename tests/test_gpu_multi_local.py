@@ -43,33 +43,38 @@ def horizon(n):
     return 0.1 / 64, 2 ** 11, 2 ** 7
 
 
-def run_group(n, Np, K, W, tol=0.0, flags=0, calls=2, nf=None, nc=None, T=None):
-    """All W ranks of one pr_local_group on cuda:0; returns the last rank's
-    (u_T, defects) per call, per-rank iteration counts and the serial fine u_ref."""
+def run_group(n, Np, K, W, tol=0.0, flags=0, calls=2, nf=None, nc=None, T=None, devices=None):
+    """All W ranks of one pr_local_group (on cuda:0, or rank r on devices[r]); returns the
+    last rank's (u_T, defects) per call, per-rank iteration counts and the serial fine u_ref."""
     T0, Nt, NC = horizon(n)
     if T is not None:
         T0 = T
     if nf is not None:
         Nt, NC = nf * Np, nc * Np
-    grids = [pr.Grid(pr.Problem(n, T=T0), 0) for _ in range(W)]
+    devices = devices or [0] * W
+    grids = [pr.Grid(pr.Problem(n, T=T0), devices[r]) for r in range(W)]
     pr.pr_local_group(grids)
-    u0 = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
-    pr.pr_fill_sine(grids[0], u0)
-    uf = torch.empty_like(u0)
-    pr.pr_fine(grids[-1], u0, uf, 0, Nt, T0 / Nt)
+    u0 = torch.empty((n, n, n), dtype=torch.float64, device="cuda:0")
+    with pr.Grid(pr.Problem(n, T=T0), 0) as g0:
+        pr.pr_fill_sine(g0, u0)
+        uf = torch.empty_like(u0)
+        pr.pr_fine(g0, u0, uf, 0, Nt, T0 / Nt)
     torch.cuda.synchronize()
+    # every rank's own copy of u0 on its device; the last rank's u_ref there too
+    u0s = [u0.to(f"cuda:{d}") for d in devices]
+    ufl = uf.to(f"cuda:{devices[-1]}")
     cfg = pr.PararealCfg(Np, NC // Np, Nt // Np, K, flags=flags, tol=tol)
     outs = [[None] * calls for _ in range(W)]
     iters = [[None] * calls for _ in range(W)]
     errs = [None] * W
-    streams = [torch.cuda.Stream() for _ in range(W)]
+    streams = [torch.cuda.Stream(device=f"cuda:{d}") for d in devices]
 
     def worker(r):
         try:
             last = r == W - 1
             for c in range(calls):
-                uT = torch.empty_like(u0) if last else None
-                d = pr.pr_parareal(grids[r], cfg, u0, uT, uf if last else None,
+                uT = torch.empty_like(u0s[r]) if last else None
+                d = pr.pr_parareal(grids[r], cfg, u0s[r], uT, ufl if last else None,
                                    stream=streams[r].cuda_stream)
                 iters[r][c] = pr.pr_last_monitors(grids[r])[1]
                 outs[r][c] = (uT, d)
@@ -91,7 +96,8 @@ def run_group(n, Np, K, W, tol=0.0, flags=0, calls=2, nf=None, nc=None, T=None):
         it1 = pr.pr_last_monitors(g1)[1]
     for g in grids:
         g.destroy()
-    return outs[W - 1], [iters[r][0] for r in range(W)], (uT1, d1, it1), uf, (T0, Nt, NC)
+    res = [(uT.to("cuda:0"), d) for uT, d in outs[W - 1]]
+    return res, [iters[r][0] for r in range(W)], (uT1, d1, it1), uf, (T0, Nt, NC)
 
 
 def same(a, b):
@@ -188,3 +194,23 @@ def test_stuck_successor_fails_with_rank_and_iteration(monkeypatch):
     e = _lone_rank(2, 0, monkeypatch)
     assert e.status == pr._lib.PR_ENCCL
     assert "rank 0, iteration 0" in str(e) and "rank 1" in str(e), str(e)
+
+
+@pytest.mark.parametrize("per_gpu", [1, 2])
+def test_local_group_across_gpus(per_gpu):
+    """One process driving ranks on several GPUs (rank r on device r % G): the
+    correction kernel stores the hand-off into the next GPU's memory through a peer
+    mapping (cudaDeviceEnablePeerAccess); with 2 ranks per GPU the 8-rank executor
+    of an 8-GPU run is exercised on a 4-GPU box.  Bitwise the 1-rank run; oracle."""
+    G = torch.cuda.device_count()
+    if G < 2:
+        pytest.skip("needs 2 GPUs")
+    W = G * per_gpu
+    res, _, (uT1, d1, _), _, (T, Nt, NC) = run_group(32, W, 3, W, devices=[r % G for r in range(W)])
+    for uT, d in res:
+        assert torch.equal(uT, uT1) and same(d, d1)
+    p = oracle.Problem(32, T=T)
+    o0 = oracle.initial(32)
+    ref = oracle.parareal(p, W, NC // W, Nt // W, 3, o0, oracle.serial_fine(p, Nt, o0))
+    err = float(np.max(np.abs(res[0][0].cpu().numpy() - ref.u_T)) / np.max(np.abs(ref.u_T)))
+    assert err <= 1e-12, err

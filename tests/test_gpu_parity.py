@@ -259,8 +259,8 @@ def test_fused_variants_bitwise(variant, monkeypatch):
 @pytest.mark.parametrize("variant", ["14", "23"])
 @pytest.mark.parametrize("n", [128, 256])
 def test_weights_as_parameters_bitwise(n, variant, monkeypatch):
-    """Direct launches with the stage weights as kernel parameters (PR_WPARAM=1, the
-    default at n >= 128) give the bits of the CUDA-graph path that reads the weights
+    """Direct launches with the stage weights as kernel parameters (PR_WPARAM=1) give
+    the bits of the CUDA-graph path (the default) that reads the weights
     from the device nu table (PR_WPARAM=0): fine_weights13 rounds every operation
     separately on host and device.  Odd and even step counts, in place and not."""
     u0 = dev(random_field(n, 61))
@@ -439,3 +439,22 @@ def test_concurrent_slices_bitwise(n, Np, K, monkeypatch):
         res.append((uT, d))
         g.destroy()
     assert torch.equal(res[0][0], res[1][0]) and res[0][1] == res[1][1]
+
+
+def test_nu_table_growth_keeps_graphs_consistent():
+    """after a short pr_fine has cached CUDA graphs, a call long enough to
+    outgrow the fine nu table (> 2^18 steps) reallocates it; every graph that captured
+    the old table must be dropped (fused graphs included).  The long run must give the
+    bits of the same run on a fresh grid."""
+    n, steps, dt = 32, 270000, 2e-7
+    u0 = dev(random_field(n, 71))
+    g = pr.Grid(pr.Problem(n, c=PARITY_C))
+    out = torch.empty_like(u0)
+    pr.pr_fine(g, u0, out, 0, 64, dt)       # caches graphs on `out` with the first table
+    pr.pr_fine(g, u0, out, 0, steps, dt)    # table grows past 1 << 20 doubles
+    with pr.Grid(pr.Problem(n, c=PARITY_C)) as g2:
+        ref = torch.empty_like(u0)
+        pr.pr_fine(g2, u0, ref, 0, steps, dt)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    g.destroy()
