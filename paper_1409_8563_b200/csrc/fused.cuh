@@ -214,10 +214,15 @@ __device__ __forceinline__ double2 apply_pair(const Weights &W, double2 L, doubl
 // compute warps finish the current one (no per-item pipeline fill).  Aux planes
 // (K_B) share the slot index of the input element they ride with.
 template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_, int PW_ = 1, int FILL_ = 0,
-          int UIN_ = 0, int DEPTHA_ = DEPTH_, int TM_ = 0>
+          int UIN_ = 0, int DEPTHA_ = DEPTH_, int TM_ = 0, int DIAG_ = 0>
 struct FusedCfgP {
+    // DIAG (timing diagnostics only, results are garbage): 1 = consumers never wait for the
+    // input ring after its first fill (compute-only upper bound); 2 = in addition stage A
+    // and stage B never wait for each other
+    static constexpr int DIAG = DIAG_;
     static constexpr bool COMB = false;  // comb.cuh configs: stage B in the stage-A lanes
     static constexpr bool WP = false;    // weights from the nu table (graph replays)
+    static constexpr bool Z2 = false;    // z2.cuh: two z planes per consumer iteration
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = 1, XP = 2,
                          PROD = 1, PW = PW_;  // PW producer warps
     // FILL 0: every plane by 16-byte cp.async; 2: planes of tiles away from the
@@ -280,6 +285,10 @@ using FusedT32 = FusedCfgP<32, 7, 4, 4, 4, 2, 2, 0, 7>;
 using FusedT32B = FusedCfgP<32, 5, 3, 4, 4, 2, 2, 0, 5>;  // K_B at 32x32: shallower rings to fit
 // 32x16 tile with the stage A -> stage B per-point hand-off through tensor memory
 using FusedTM = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 1>;
+// timing diagnostics (garbage results): no input waits / no waits at all (PR_FTILE 26 / 27)
+using FusedD1 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 0, 1>;
+using FusedD2 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 0, 2>;
+using FusedD3 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 0, 3>;  // every tile by TMA (PR_FTILE 28)
 // the same kernel with the two stages' weights passed as launch parameters (direct launches):
 // they sit in uniform registers / the constant bank instead of 26 registers per thread
 template <class C> struct WithWP : C { static constexpr bool WP = true; };
@@ -406,12 +415,16 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
             }
         }
         // TMA fills for tiles whose boxes stay inside the field (no periodic seam)
-        const bool tma = C::FILL == 2 && w.x0 >= C::HX && w.x0 - C::HX + IW <= n &&
-                         w.y0 >= C::HY && w.y0 - C::HY + C::IH <= n &&
-                         (KB == K_A || w.x0 - 2 + EW <= n);
+        // (DIAG 3, timing only: every tile by TMA, zero-filled instead of wrapped at the seams)
+        const bool tma = C::FILL == 2 && ((w.x0 >= C::HX && w.x0 - C::HX + IW <= n &&
+                                           w.y0 >= C::HY && w.y0 - C::HY + C::IH <= n &&
+                                           (KB == K_A || w.x0 - 2 + EW <= n)) || C::DIAG == 3);
         int zin = wrap1(w.z_begin - C::HZ, n);
 #pragma unroll 1
         for (int e = 0; e < E; ++e) {
+            if constexpr (C::DIAG == 1 || C::DIAG == 2) {
+                if (pos.round > 0) break;  // only the first fill
+            }
             if (pos.round > 0) mbar_wait(&in_empty[pos.slot], (pos.round - 1) & 1);
             if constexpr (C::FILL == 2) {
                 if (tma) {
@@ -528,7 +541,7 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
         RingPos p0 = base;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            mbar_wait(&in_full[p0.slot], p0.round & 1);
+            if ((C::DIAG != 1 && C::DIAG != 2) || p0.round == 0) mbar_wait(&in_full[p0.slot], p0.round & 1);
             const double *ys = yring + size_t(p0.slot) * C::Y_ELEMS + sY;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) q[r][e] = lds2(ys + r * IW);
@@ -540,7 +553,7 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
         RingPos p2 = ring_at(base, 2, DEPTH), p4 = p0;  // elements j+2, j+4
         rotating_loop(NJ, [&](auto ph, int j) {
             constexpr int P = decltype(ph)::value;
-            mbar_wait(&in_full[p4.slot], p4.round & 1);  // element j+4 (+ aux j) landed
+            if ((C::DIAG != 1 && C::DIAG != 2) || p4.round == 0) mbar_wait(&in_full[p4.slot], p4.round & 1);  // element j+4 (+ aux j) landed
             const double *yq = yring + size_t(p4.slot) * C::Y_ELEMS + sY;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = lds2(yq + r * IW);
@@ -575,7 +588,7 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                     acv[r] = lds2(au + C::Z_ELEMS + (need ? tp0 + r * TXO : 0));
                 }
             }
-            if (zpos.round > 0) mbar_wait(&empty[zpos.slot], (zpos.round - 1) & 1);
+            if (C::DIAG != 2 && zpos.round > 0) mbar_wait(&empty[zpos.slot], (zpos.round - 1) & 1);
             double *zs = zring + size_t(zpos.slot) * ZS;
             if constexpr (C::TM) {
                 if (tile_lane) {  // intermediate centre, t0 (and u) of this plane -> TMEM
@@ -711,7 +724,7 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
         RingPos zc_pos = zq_pos;  // Z plane j-2 (valid from j = 2)
         rotating_loop(NJ, [&](auto ph, int j) {
             constexpr int P = decltype(ph)::value;
-            mbar_wait(&full[zq_pos.slot], zq_pos.round & 1);
+            if (C::DIAG != 2) mbar_wait(&full[zq_pos.slot], zq_pos.round & 1);
             if constexpr (C::TM) {
                 tm_fence_after();
                 TmRaw8 tz;
@@ -806,6 +819,7 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
 // stencil_kernel<K_COARSE> (bitwise identical results).
 template <int TYO_, int DEPTH_, int RPT_, int PW_, int FILL_>
 struct CoarseCfgP {
+    static constexpr int DIAG = 0;
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, RPT = RPT_, PW = PW_, FILL = FILL_;
     static constexpr int HX = 2, HY = 1, HZ = 1;  // radius-1 stencil; x halo pair-aligned
     static constexpr int IW = TXO + 2 * HX, IH = TYO + 2 * HY, IWS = IW;

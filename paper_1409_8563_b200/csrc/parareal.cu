@@ -29,6 +29,12 @@
 #include "fused.cuh"
 #include "comb.cuh"
 #include "onestep.cuh"
+#include "z2.cuh"
+
+namespace prk {
+// two z planes per consumer iteration: 6-slot intermediate ring; K_A input ring 9 slots, K_B 8
+using FusedZ2 = WithZ2<FusedCfgP<16, 8, 6, 2, 2, 2, 2, 0, 9>>;
+}  // namespace prk
 
 using namespace prk;
 
@@ -301,6 +307,7 @@ template <int KB, class C>
 static constexpr auto fused_kernel_of() {
     if constexpr (std::is_same_v<C, OneCfg>) return &onestep_kernel<KB, C>;
     else if constexpr (C::COMB) return &fused_comb_kernel<KB, C>;
+    else if constexpr (C::Z2) return &fused_z2_kernel<KB, C>;
     else return &fused_persist_kernel<KB, C>;
 }
 
@@ -329,6 +336,9 @@ static pr_status setup_fused_persist(pr_grid *g) {
     const int slots = g->sms * occ;
     const int ch = pick_chunks(n, c.tiles_x * c.tiles_y, slots, std::is_same_v<C, OneCfg> ? 8 : 4);
     c.cz = (n + ch - 1) / ch;
+    if constexpr (!std::is_same_v<C, OneCfg>) {
+        if constexpr (C::Z2) c.cz = (c.cz + 1) & ~1;  // two planes per iteration: even chunks
+    }
     c.chunks_z = (n + c.cz - 1) / c.cz;
     const int items = c.tiles_x * c.tiles_y * c.chunks_z;
     c.blocks = std::min(items, slots);  // persistent: one CTA per resident slot
@@ -393,13 +403,15 @@ static void launch_coarse_persist(pr_grid *g, const StencilArgs &a0, cudaStream_
 // (K_A: stages 1+2, K_B: stages 3+4; they are independent launches over the whole
 // grid, so their tilings may differ).  X(id, config of K_A, config of K_B)
 #define PRK_FVARIANTS(X) \
-    X(14, FusedP4, FusedP4) X(20, FusedT32, FusedP4) X(21, FusedT32, FusedT32B) X(22, Comb16, Comb16) \
-    X(23, FusedTM, FusedTM) X(24, OneCfg, OneCfg)
+    X(14, FusedP4, FusedP4) X(22, Comb16, Comb16) X(23, FusedTM, FusedTM) X(24, OneCfg, OneCfg) \
+    X(25, FusedZ2, FusedZ2)
 #ifdef PRK_VARIANTS
+// tuning history and timing diagnostics (26-28 give garbage results by design)
 #define PRK_FVARIANTS_OLD(X)                                                                    \
     X(10, FusedP0, FusedP0) X(11, FusedP1, FusedP1) X(12, FusedP2, FusedP2) X(13, FusedP3, FusedP3) \
     X(15, FusedP5, FusedP5) X(16, FusedP6, FusedP6) X(17, FusedP7, FusedP7) X(18, FusedP8, FusedP8) \
-    X(19, FusedP9, FusedP9)
+    X(19, FusedP9, FusedP9) X(20, FusedT32, FusedP4) X(21, FusedT32, FusedT32B)                    \
+    X(26, FusedD1, FusedD1) X(27, FusedD2, FusedD2) X(28, FusedD3, FusedD3)
 #else
 #define PRK_FVARIANTS_OLD(X)
 #endif
@@ -417,7 +429,7 @@ static void fused_tiles(int v, int *tya, int *tyb) {
 }
 
 // variants that also exist with the weights as launch parameters (WithWP)
-#define PRK_FVARIANTS_WP(X) X(14, FusedP4, FusedP4) X(23, FusedTM, FusedTM)
+#define PRK_FVARIANTS_WP(X) X(14, FusedP4, FusedP4) X(23, FusedTM, FusedTM) X(25, FusedZ2, FusedZ2)
 static bool fused_has_wp(int v) {
     switch (v) {
 #define X(id, A, B) case id: return true;
@@ -1018,7 +1030,8 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
         // batches reading the nu table.  Measured neutral at 256^3 / 512^3 and 9 % slower
         // at 128^3 (launch gaps), so the graphs stay the default.
         const char *we = getenv("PR_WPARAM");
-        g->wparam = g->f2 && !g->f1 && fused_has_wp(g->fvariant) && we && we[0] == '1';
+        g->wparam = g->f2 && !g->f1 && fused_has_wp(g->fvariant) &&
+                    (we ? we[0] == '1' : g->fvariant == 25);  // z2 pays its registers with WP
     }
     if (g->f2) {
         if ((s = setup_fused<K_A>(g)) != PR_OK) return bail(s);
