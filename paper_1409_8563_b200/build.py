@@ -13,6 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libparareal.so")
 LIB_DEBUG = os.path.join(HERE, "libparareal_debug.so")  # PRK_DEBUG: in-kernel index checks
+# PRK_VARIANTS: tuning-history variants and timing diagnostics (select with PR_LIB=<path>)
+LIB_VARIANTS = os.path.join(HERE, "libparareal_variants.so")
 SRCS = [os.path.join(HERE, "csrc", "parareal.cu")]
 DEPS = SRCS + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "parareal.h")]
 
@@ -32,22 +34,22 @@ def nccl_dirs():
     return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
-def nvcc_cmd(out: str, debug: bool = False) -> list[str]:
+def nvcc_cmd(out: str, debug: bool = False, variants: bool = False) -> list[str]:
     inc, lib = nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     return [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
             "-std=c++17", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-shared", "-Xptxas", "-v",
-            *(["-DPRK_DEBUG"] if debug else []),
+            *(["-DPRK_DEBUG"] if debug else []), *(["-DPRK_VARIANTS"] if variants else []),
             "-I", os.path.join(ROOT, "include"), "-I", inc,
             *SRCS, "-o", out, "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}"]
 
 
-def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
-    lib = LIB_DEBUG if debug else LIB
+def build(force: bool = False, verbose: bool = False, debug: bool = False, variants: bool = False) -> str:
+    lib = LIB_DEBUG if debug else LIB_VARIANTS if variants else LIB
     if not force and os.path.exists(lib) and os.path.getmtime(lib) >= max(os.path.getmtime(d) for d in DEPS):
         return lib
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = nvcc_cmd(tmp, debug)
+    cmd = nvcc_cmd(tmp, debug, variants)
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

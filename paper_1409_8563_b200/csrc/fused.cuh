@@ -218,7 +218,7 @@ template <int TYO_, int DEPTH_, int ZD_, int RPTA_, int RPTB_, int PW_ = 1, int 
 struct FusedCfgP {
     // DIAG (timing diagnostics only, results are garbage): 1 = consumers never wait for the
     // input ring after its first fill (compute-only upper bound); 2 = in addition stage A
-    // and stage B never wait for each other
+    // and stage B never wait for each other; 3 = every tile by TMA
     static constexpr int DIAG = DIAG_;
     static constexpr bool COMB = false;  // comb.cuh configs: stage B in the stage-A lanes
     static constexpr bool WP = false;    // weights from the nu table (graph replays)
