@@ -109,7 +109,13 @@ pr_status pr_destroy_grid(pr_grid *grid);
  * allowed; any other overlap is PR_EINVAL.  n_steps = 0 copies.  One step is
  * two fused kernels (stages 1+2 and 3+4, 56 B/point) when n is a multiple of
  * 32, else four fused stage passes (128 B/point); both give bitwise identical
- * results.  Asynchronous on `stream` for device pointers. */
+ * results.  The environment variable PR_FTILE (read at
+ * pr_create_grid) selects an alternative design of the two-kernel step, all
+ * bitwise identical: 22 stage B in the stage-A lanes, 23 the stage hand-off
+ * through tensor memory, 24 the whole step in ONE kernel (16 B/point), 25 two z
+ * planes per warp iteration; PR_WPARAM=1 launches the fused kernels directly
+ * with the stage weights as launch parameters instead of CUDA-graph batches.
+ * Asynchronous on `stream` for device pointers. */
 pr_status pr_fine(pr_grid *grid, const double *u_in, double *u_out, int64_t step0,
                   int64_t n_steps, double dt, void *stream);
 
@@ -235,10 +241,11 @@ pr_status pr_last_monitors(pr_grid *grid, double *changes, int32_t cap, int32_t 
 pr_status pr_last_timings(pr_grid *grid, double *out, int32_t cap);
 
 /* Static facts about a grid's launch configuration (no GPU work):
- *   fine_kernels_per_step: 2 (fused S1+S2 / S3+S4 kernels, tile-aligned n) or
+ *   fine_kernels_per_step: 2 (fused S1+S2 / S3+S4 kernels, tile-aligned n),
+ *                          1 (PR_FTILE=24: one kernel per step) or
  *                          4 (one fused pass per RK4 stage);
- *   fine_bytes_per_point:  algorithmic HBM bytes per grid point per RK4 step
- *                          (56 or 128);
+ *   fine_bytes_per_point:  HBM bytes per grid point per RK4 step that path must
+ *                          move (56, 16 or 128);
  *   coarse_bytes_per_point: 16 (one Euler pass). */
 typedef struct {
     int32_t fine_kernels_per_step;
