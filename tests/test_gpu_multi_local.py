@@ -214,3 +214,28 @@ def test_local_group_across_gpus(per_gpu):
     ref = oracle.parareal(p, W, NC // W, Nt // W, 3, o0, oracle.serial_fine(p, Nt, o0))
     err = float(np.max(np.abs(res[0][0].cpu().numpy() - ref.u_T)) / np.max(np.abs(ref.u_T)))
     assert err <= 1e-12, err
+
+
+def test_local_group_argument_errors():
+    """pr_local_group rejects an empty group and a grid listed twice (PR_EINVAL)."""
+    g = pr.Grid(pr.Problem(32), 0)
+    with pytest.raises(pr.PrError) as ei:
+        pr.pr_local_group([g, g])
+    assert ei.value.status == pr._lib.PR_EINVAL
+    with pytest.raises(pr.PrError) as ei:
+        pr.pr_local_group([])
+    assert ei.value.status == pr._lib.PR_EINVAL
+    g.destroy()
+
+
+def test_local_group_rank_count_must_divide_slices():
+    """N_p must be a multiple of the group size, as with NCCL ranks (PR_EINVAL)."""
+    grids = [pr.Grid(pr.Problem(32), 0) for _ in range(3)]
+    pr.pr_local_group(grids)
+    u0 = torch.empty((32, 32, 32), dtype=torch.float64, device="cuda")
+    pr.pr_fill_sine(grids[0], u0)
+    with pytest.raises(pr.PrError) as ei:
+        pr.pr_parareal(grids[0], pr.PararealCfg(4, 4, 16, 1), u0, None, None)
+    assert ei.value.status == pr._lib.PR_EINVAL
+    for g in grids:
+        g.destroy()
