@@ -281,6 +281,9 @@ struct FusedCfgP {
 using FusedP4 = FusedCfgP<16, 9, 4, 2, 2, 2, 2>;  // 32x16 tile, TMA tensor fills (default, PR_FTILE=14)
 // 32x32 output tile, four rows per lane in both stages (12 warps): stage A's halo ring
 // recomputes 27 % instead of 41 %, and each lane reads 2 instead of 2.5 shared values per point
+// power-of-two ring depths: ring positions as masked counters (K_A 16 input slots, K_B 8)
+using FusedQ16 = FusedCfgP<16, 8, 4, 2, 2, 2, 2, 0, 16>;
+using FusedQ8 = FusedCfgP<16, 8, 4, 2, 2, 2, 2, 0, 8>;
 using FusedT32 = FusedCfgP<32, 7, 4, 4, 4, 2, 2, 0, 7>;
 using FusedT32B = FusedCfgP<32, 5, 3, 4, 4, 2, 2, 0, 5>;  // K_B at 32x32: shallower rings to fit
 // 32x16 tile with the stage A -> stage B per-point hand-off through tensor memory
@@ -337,6 +340,29 @@ __device__ __forceinline__ RingPos ring_at(RingPos p, int k, int depth) {
     return p;
 }
 
+// ring position of a D-slot ring as a running counter: for power-of-two D the slot
+// and round are a mask and a shift of it (fewer integer instructions per pipeline
+// step than the incremental slot/round pair, which other depths keep)
+template <int D, bool P2 = (D & (D - 1)) == 0> struct RingP;
+template <int D> struct RingP<D, true> {
+    unsigned c = 0;
+    __device__ __forceinline__ int slot() const { return int(c & unsigned(D - 1)); }
+    __device__ __forceinline__ int round() const { return int(c / unsigned(D)); }
+    __device__ __forceinline__ void step() { ++c; }
+    __device__ __forceinline__ RingP at(int k) const { RingP r; r.c = c + unsigned(k); return r; }
+};
+template <int D> struct RingP<D, false> {
+    int s = 0, r = 0;
+    __device__ __forceinline__ int slot() const { return s; }
+    __device__ __forceinline__ int round() const { return r; }
+    __device__ __forceinline__ void step() { if (++s == D) { s = 0; ++r; } }
+    __device__ __forceinline__ RingP at(int k) const {
+        RingP q = *this;
+        for (int i = 0; i < k; ++i) q.step();
+        return q;
+    }
+};
+
 // Chunk c (16 bytes) of a rows x (mid + 2 hc)-chunk tile plane -> (row, chunk column),
 // ordered so that eight consecutive producer lanes fetch one aligned 128-byte
 // global line: first the mid chunks of every row (the tile's own x range, 256-byte
@@ -366,7 +392,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
     // 0 .. NP-1 (NTA + NTB is a multiple of 32, so the % keeps the range visible)
     const int lane = (threadIdx.x - (C::NTA + C::NTB)) % NP;
     const uint32_t yring_s = smem_u32(yring), aring_s = smem_u32(aring);
-    RingPos pos;
+    RingP<DEPTH> pos;
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const WorkItem w = decode_item(a, item, TXO, C::TYO);
@@ -423,36 +449,36 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
 #pragma unroll 1
         for (int e = 0; e < E; ++e) {
             if constexpr (C::DIAG == 1 || C::DIAG == 2) {
-                if (pos.round > 0) break;  // only the first fill
+                if (pos.round() > 0) break;  // only the first fill
             }
-            if (pos.round > 0) mbar_wait(&in_empty[pos.slot], (pos.round - 1) & 1);
+            if (pos.round() > 0) mbar_wait(&in_empty[pos.slot()], (pos.round() - 1) & 1);
             if constexpr (C::FILL == 2) {
                 if (tma) {
                     if (lane == 0) {
-                        uint64_t *bar = &in_full[pos.slot];
+                        uint64_t *bar = &in_full[pos.slot()];
                         const int j = e - 4;
                         const bool ua = KB == K_B && j >= 0 && j < NJ;
                         const bool ca = ua && j >= 2 && j < w.nz + 2;
                         mbar_expect_tx(bar, 8u * (C::IH * IW + (ua ? C::EH * EW : 0) +
                                                   (ca ? C::T_ELEMS : 0)));
-                        tma_load3(yring_s + uint32_t(pos.slot) * (C::Y_ELEMS * 8), &tm->y,
+                        tma_load3(yring_s + uint32_t(pos.slot()) * (C::Y_ELEMS * 8), &tm->y,
                                   w.x0 - C::HX, w.y0 - C::HY, zin, bar);
                         if (ua) {
                             const int zaux = zin >= 2 ? zin - 2 : zin - 2 + n;
-                            const uint32_t dst = aring_s + uint32_t(pos.slot) * (C::AUX_ELEMS * 8);
+                            const uint32_t dst = aring_s + uint32_t(pos.slot()) * (C::AUX_ELEMS * 8);
                             tma_load3(dst, &tm->u, w.x0 - 2, w.y0 - 2, zaux, bar);
                             if (ca) tma_load3(dst + 8 * C::Z_ELEMS, &tm->c, w.x0, w.y0, zaux, bar);
                         }
                     }
-                    cp_async_mbar_arrive(&in_full[pos.slot]);
+                    cp_async_mbar_arrive(&in_full[pos.slot()]);
                     zin = (zin + 1 == n) ? 0 : zin + 1;
-                    pos.step(DEPTH);
+                    pos.step();
                     continue;
                 }
             }
             {
                 const double *src = a.y + size_t(zin) * nn;
-                const uint32_t dst = yring_s + uint32_t(pos.slot) * (C::Y_ELEMS * 8);
+                const uint32_t dst = yring_s + uint32_t(pos.slot()) * (C::Y_ELEMS * 8);
 #pragma unroll
                 for (int k = 0; k < NY; ++k)
                     if (ysrc[k] >= 0) cp_async16s(dst + ydst[k], src + ysrc[k]);
@@ -463,7 +489,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
                     int zaux = zin - 2;
                     if (zaux < 0) zaux += n;
                     const size_t pl = size_t(zaux) * nn;
-                    const uint32_t dst = aring_s + uint32_t(pos.slot) * (C::AUX_ELEMS * 8);
+                    const uint32_t dst = aring_s + uint32_t(pos.slot()) * (C::AUX_ELEMS * 8);
 #pragma unroll
                     for (int k = 0; k < NU; ++k)
                         if (usrc[k] >= 0) cp_async16s(dst + udst[k], a.p0 + pl + usrc[k]);
@@ -474,9 +500,9 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
                     }
                 }
             }
-            cp_async_mbar_arrive(&in_full[pos.slot]);
+            cp_async_mbar_arrive(&in_full[pos.slot()]);
             zin = (zin + 1 == n) ? 0 : zin + 1;
-            pos.step(DEPTH);
+            pos.step();
         }
     }
     cp_async_wait<0>();
@@ -532,39 +558,40 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
     const bool tcol = l >= 1 && l <= TXO / 2;
     const int tp0 = (r0 - 2) * TXO + 2 * l - 2;
 
-    RingPos base, zpos;  // input element 0 of the current item; next Z plane
+    RingP<DEPTH> base;  // input element 0 of the current item
+    RingP<ZD> zpos;     // next Z plane
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const WorkItem w = decode_item(a, item, TXO, C::TYO);
         const int NJ = w.nz + 4;
         double2 q[RPT][5];
-        RingPos p0 = base;
+        RingP<DEPTH> p0 = base;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            if ((C::DIAG != 1 && C::DIAG != 2) || p0.round == 0) mbar_wait(&in_full[p0.slot], p0.round & 1);
-            const double *ys = yring + size_t(p0.slot) * C::Y_ELEMS + sY;
+            if ((C::DIAG != 1 && C::DIAG != 2) || p0.round() == 0) mbar_wait(&in_full[p0.slot()], p0.round() & 1);
+            const double *ys = yring + size_t(p0.slot()) * C::Y_ELEMS + sY;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) q[r][e] = lds2(ys + r * IW);
-            p0.step(DEPTH);
+            p0.step();
         }
         // elements 0 and 1 were only needed for the queue
-        mbar_arrive(&in_empty[base.slot]);
-        mbar_arrive(&in_empty[ring_at(base, 1, DEPTH).slot]);
-        RingPos p2 = ring_at(base, 2, DEPTH), p4 = p0;  // elements j+2, j+4
+        mbar_arrive(&in_empty[base.slot()]);
+        mbar_arrive(&in_empty[base.at(1).slot()]);
+        RingP<DEPTH> p2 = base.at(2), p4 = p0;  // elements j+2, j+4
         rotating_loop(NJ, [&](auto ph, int j) {
             constexpr int P = decltype(ph)::value;
-            if ((C::DIAG != 1 && C::DIAG != 2) || p4.round == 0) mbar_wait(&in_full[p4.slot], p4.round & 1);  // element j+4 (+ aux j) landed
-            const double *yq = yring + size_t(p4.slot) * C::Y_ELEMS + sY;
+            if ((C::DIAG != 1 && C::DIAG != 2) || p4.round() == 0) mbar_wait(&in_full[p4.slot()], p4.round() & 1);  // element j+4 (+ aux j) landed
+            const double *yq = yring + size_t(p4.slot()) * C::Y_ELEMS + sY;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = lds2(yq + r * IW);
-            const double *ys = yring + size_t(p2.slot) * C::Y_ELEMS + sY;
+            const double *ys = yring + size_t(p2.slot()) * C::Y_ELEMS + sY;
             double2 col[RPT + 4];
 #pragma unroll
             for (int r = 0; r < RPT + 4; ++r)
                 col[r] = (r >= 2 && r < RPT + 2) ? q[r - 2][(P + 2) % 5] : lds2(ys + (r - 2) * IW);
             // K_B: u on the ring is in shared memory already; load it before the
             // stencil so its latency hides under the FMAs
-            const double *au = aring + size_t(p4.slot) * C::AUX_ELEMS;  // aux j
+            const double *au = aring + size_t(p4.slot()) * C::AUX_ELEMS;  // aux j
             [[maybe_unused]] const bool outp = j >= 2 && j < w.nz + 2;
             double2 ubv[KB == K_B ? RPT : 1];
             if constexpr (KB == K_B) {
@@ -588,8 +615,8 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                     acv[r] = lds2(au + C::Z_ELEMS + (need ? tp0 + r * TXO : 0));
                 }
             }
-            if (C::DIAG != 2 && zpos.round > 0) mbar_wait(&empty[zpos.slot], (zpos.round - 1) & 1);
-            double *zs = zring + size_t(zpos.slot) * ZS;
+            if (C::DIAG != 2 && zpos.round() > 0) mbar_wait(&empty[zpos.slot()], (zpos.round() - 1) & 1);
+            double *zs = zring + size_t(zpos.slot()) * ZS;
             if constexpr (C::TM) {
                 if (tile_lane) {  // intermediate centre, t0 (and u) of this plane -> TMEM
                     tm_fence_after();
@@ -611,7 +638,7 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                         }
                         sts2(zs + sZ + r * EW, zz[r]);  // x/y neighbours for stage B
                     }
-                    const uint32_t col = tq_addr + uint32_t(zpos.slot * C::TM_PLANE);
+                    const uint32_t col = tq_addr + uint32_t(zpos.slot() * C::TM_PLANE);
                     tm_st8(col, zz[0], zz[1]);
                     tm_st8(col + 8, t0v[0], t0v[1]);
                     if (KB == K_A) tm_st8(col + 16, q[0][(P + 2) % 5], q[1][(P + 2) % 5]);
@@ -667,16 +694,16 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                     }
                 }
             }
-            mbar_arrive(&full[zpos.slot]);
-            mbar_arrive(&in_empty[p2.slot]);  // element j+2 done (aux j lives in slot j+4)
-            p2.step(DEPTH);
-            p4.step(DEPTH);
-            zpos.step(ZD);
+            mbar_arrive(&full[zpos.slot()]);
+            mbar_arrive(&in_empty[p2.slot()]);  // element j+2 done (aux j lives in slot j+4)
+            p2.step();
+            p4.step();
+            zpos.step();
         });
         // the item's last two input elements were only used by the queue
-        mbar_arrive(&in_empty[p2.slot]);
-        mbar_arrive(&in_empty[ring_at(p2, 1, DEPTH).slot]);
-        base = ring_at(p2, 2, DEPTH);
+        mbar_arrive(&in_empty[p2.slot()]);
+        mbar_arrive(&in_empty[p2.at(1).slot()]);
+        base = p2.at(2);
     }
 }
 
@@ -711,8 +738,8 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
     }
     const double dt = a.dt;
 
-    RingPos zq_pos;  // Z plane j of the current item
-    RingPos in_pos;  // UIN: input element j of the current item
+    RingP<ZD> zq_pos;     // Z plane j of the current item
+    RingP<DEPTH> in_pos;  // UIN: input element j of the current item
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const WorkItem w = decode_item(a, item, TXO, C::TYO);
@@ -721,24 +748,24 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
         double *o1 = KB == K_A ? a.o1 + size_t(w.z_begin) * nn + size_t(w.y0 + r0) * n + w.x0 + 2 * m
                                : nullptr;
         double2 q[RPT][5];
-        RingPos zc_pos = zq_pos;  // Z plane j-2 (valid from j = 2)
+        RingP<ZD> zc_pos = zq_pos;  // Z plane j-2 (valid from j = 2)
         rotating_loop(NJ, [&](auto ph, int j) {
             constexpr int P = decltype(ph)::value;
-            if (C::DIAG != 2) mbar_wait(&full[zq_pos.slot], zq_pos.round & 1);
+            if (C::DIAG != 2) mbar_wait(&full[zq_pos.slot()], zq_pos.round() & 1);
             if constexpr (C::TM) {
                 tm_fence_after();
                 TmRaw8 tz;
-                tm_ld8(tq_addr + uint32_t(zq_pos.slot * C::TM_PLANE), tz);  // own centre, plane j
+                tm_ld8(tq_addr + uint32_t(zq_pos.slot() * C::TM_PLANE), tz);  // own centre, plane j
                 tm_wait_ld();
 #pragma unroll
                 for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = tm_row(tz, r);
             } else {
-                const double *zq = zring + size_t(zq_pos.slot) * ZS + sZ;
+                const double *zq = zring + size_t(zq_pos.slot()) * ZS + sZ;
 #pragma unroll
                 for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = lds2(zq + r * EW);
             }
             if (j >= 4 && valid) {
-                const double *zs = zring + size_t(zc_pos.slot) * ZS;
+                const double *zs = zring + size_t(zc_pos.slot()) * ZS;
                 const double *zc = zs + sZ;
                 double2 col[RPT + 4];
 #pragma unroll
@@ -751,7 +778,7 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
                                            col[r + 3], col[r + 4], q[r]);
                 TmRaw8 tt0, tt1;  // TM: t0 and u of the output point (plane j-2)
                 if constexpr (C::TM) {
-                    const uint32_t cc = tq_addr + uint32_t(zc_pos.slot * C::TM_PLANE);
+                    const uint32_t cc = tq_addr + uint32_t(zc_pos.slot() * C::TM_PLANE);
                     tm_ld8(cc + 8, tt0);
                     if (KB == K_A) tm_ld8(cc + 16, tt1);
                     tm_wait_ld();
@@ -765,7 +792,7 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
                         // u at the output point: input element j (plane z_begin + j - 4)
                         const double2 t1 =
                             C::TM ? tm_row(tt1, r)
-                            : UIN ? lds2(yring + size_t(in_pos.slot) * C::Y_ELEMS + sU + r * C::IWS)
+                            : UIN ? lds2(yring + size_t(in_pos.slot()) * C::Y_ELEMS + sU + r * C::IWS)
                                   : lds2(zs + C::Z_ELEMS + C::T_ELEMS + sT + r * TXO);
                         double2 v0, v1;
                         v0.x = t0.x + (dt / 3.0) * kB.x;  v0.y = t0.y + (dt / 3.0) * kB.y;
@@ -786,24 +813,24 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
             }
             if (j >= 2) {
                 if constexpr (C::TM) tm_fence_before();
-                mbar_arrive(&empty[zc_pos.slot]);
-                zc_pos.step(ZD);
+                mbar_arrive(&empty[zc_pos.slot()]);
+                zc_pos.step();
             }
-            zq_pos.step(ZD);
+            zq_pos.step();
             if constexpr (UIN) {  // input element j: read above (j >= 4) or never (j < 4)
-                mbar_arrive(&in_empty[in_pos.slot]);
-                in_pos.step(DEPTH);
+                mbar_arrive(&in_empty[in_pos.slot()]);
+                in_pos.step();
             }
         });
         // release the item's last two Z planes (never a centre)
-        mbar_arrive(&empty[zc_pos.slot]);
-        zc_pos.step(ZD);
-        mbar_arrive(&empty[zc_pos.slot]);
+        mbar_arrive(&empty[zc_pos.slot()]);
+        zc_pos.step();
+        mbar_arrive(&empty[zc_pos.slot()]);
         if constexpr (UIN) {  // input elements nz+4 .. nz+7 (z halo only)
 #pragma unroll 1
             for (int e = 0; e < 4; ++e) {
-                mbar_arrive(&in_empty[in_pos.slot]);
-                in_pos.step(DEPTH);
+                mbar_arrive(&in_empty[in_pos.slot()]);
+                in_pos.step();
             }
         }
     }
@@ -882,30 +909,30 @@ __device__ __forceinline__ void stage_c_p(const StencilArgs &a, double *sm, int 
     }
     const double dt = a.dt;
 
-    RingPos base;  // input element 0 of the current item
+    RingP<DEPTH> base;  // input element 0 of the current item
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const WorkItem w = decode_item(a, item, TXO, C::TYO);
         double *o0 = a.o0 + size_t(w.z_begin) * nn + size_t(w.y0 + r0) * n + w.x0 + 2 * m;
         double2 q[RPT][3];
-        RingPos p0 = base;
+        RingP<DEPTH> p0 = base;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-            mbar_wait(&in_full[p0.slot], p0.round & 1);
-            const double *ys = yring + size_t(p0.slot) * C::Y_ELEMS + sY;
+            mbar_wait(&in_full[p0.slot()], p0.round() & 1);
+            const double *ys = yring + size_t(p0.slot()) * C::Y_ELEMS + sY;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) q[r][e] = lds2(ys + r * IW);
-            p0.step(DEPTH);
+            p0.step();
         }
-        mbar_arrive(&in_empty[base.slot]);      // element 0: queue only
-        RingPos pc = ring_at(base, 1, DEPTH), pq = p0;  // elements j+1 (centre), j+2
+        mbar_arrive(&in_empty[base.slot()]);      // element 0: queue only
+        RingP<DEPTH> pc = base.at(1), pq = p0;  // elements j+1 (centre), j+2
         rotating_loop3(w.nz, [&](auto ph, int j) {
             constexpr int P = decltype(ph)::value;  // q[.][P] = z-1, [P+1] = z, [P+2] = z+1
-            mbar_wait(&in_full[pq.slot], pq.round & 1);
-            const double *yq = yring + size_t(pq.slot) * C::Y_ELEMS + sY;
+            mbar_wait(&in_full[pq.slot()], pq.round() & 1);
+            const double *yq = yring + size_t(pq.slot()) * C::Y_ELEMS + sY;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) q[r][(P + 2) % 3] = lds2(yq + r * IW);
-            const double *ys = yring + size_t(pc.slot) * C::Y_ELEMS + sY;
+            const double *ys = yring + size_t(pc.slot()) * C::Y_ELEMS + sY;
             double2 col[RPT + 2];
 #pragma unroll
             for (int r = 0; r < RPT + 2; ++r)
@@ -938,12 +965,12 @@ __device__ __forceinline__ void stage_c_p(const StencilArgs &a, double *sm, int 
                 *reinterpret_cast<double2 *>(o0 + size_t(r) * n) = v;
             }
             o0 += nn;
-            mbar_arrive(&in_empty[pc.slot]);  // the centre plane is no longer read from smem
-            pc.step(DEPTH);
-            pq.step(DEPTH);
+            mbar_arrive(&in_empty[pc.slot()]);  // the centre plane is no longer read from smem
+            pc.step();
+            pq.step();
         });
-        mbar_arrive(&in_empty[pc.slot]);  // the item's last element (queue only)
-        base = ring_at(pc, 1, DEPTH);
+        mbar_arrive(&in_empty[pc.slot()]);  // the item's last element (queue only)
+        base = pc.at(1);
     }
 }
 
