@@ -239,3 +239,15 @@ def test_local_group_rank_count_must_divide_slices():
     assert ei.value.status == pr._lib.PR_EINVAL
     for g in grids:
         g.destroy()
+
+
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_local_liveness_sweep(W):
+    """SURVEY T5 on one GPU: every (N_p, K) with N_p in {W, 2W} and K in {0, 1, 2, 5, 8}
+    (K > N_p included) completes without a hang, bitwise equal to the 1-rank run."""
+    n = 8
+    for Np in (W, 2 * W):
+        for K in (0, 1, 2, 5, 8):
+            res, _, (uT1, d1, _), _, _ = run_group(n, Np, K, W, nf=2, nc=1, T=Np * 2 * 1e-3, calls=1)
+            uT, d = res[0]
+            assert torch.equal(uT, uT1) and same(d, d1), (W, Np, K)

@@ -458,3 +458,19 @@ def test_nu_table_growth_keeps_graphs_consistent():
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
     g.destroy()
+
+
+@pytest.mark.parametrize("nu0,omega", [(0.0, 0.0), (0.15, 0.0), (0.1, 100.0)])
+@pytest.mark.parametrize("n", [12, 32, 128])
+def test_nu_range_fine_and_coarse(n, nu0, omega):
+    """SURVEY T2's nu range: pure advection (nu = 0), a constant nu = 0.15 and the paper's
+    oscillating nu(t); the fused (n = 32, 128) and four-pass (n = 12) F paths and G
+    against the oracle, 1e-12 normwise."""
+    u0 = random_field(n, 81)
+    g = grid(n, nu0=nu0, omega=omega)
+    dt, Dt = 1e-4 * (32 / n) ** 2, 4e-4 * (32 / n) ** 2
+    out = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+    pr.pr_fine(g, dev(u0), out, 3, 19, dt)
+    assert rel(out, oracle.fine(oproblem(n, nu0=nu0, omega=omega), u0, 3, 19, dt)) <= TOL
+    pr.pr_coarse(g, dev(u0), out, 3, 7, Dt)
+    assert rel(out, oracle.coarse(oproblem(n, nu0=nu0, omega=omega), u0, 3, 7, Dt)) <= TOL
