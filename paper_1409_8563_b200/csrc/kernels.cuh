@@ -341,22 +341,33 @@ stencil_kernel(const StencilArgs a) {
         for (int r = 0; r < RPT; ++r) {
             const double *yrow = ys + r * SX;
             const double yc = q[r][R];
-            // partial sums per axis keep the dependent FMA chains short
-            double ax = wm1[0] * yrow[-1];
-            ax = fma(wp1[0], yrow[1], ax);
-            double ay = wm1[1] * col[r + R - 1];
-            ay = fma(wp1[1], col[r + R + 1], ay);
-            double az = wm1[2] * q[r][R - 1];
-            az = fma(wp1[2], q[r][R + 1], az);
+            double Lv;  // right-hand side at this point
             if constexpr (R == 2) {
-                ax = fma(wm2[0], yrow[-2], ax);
-                ax = fma(wp2[0], yrow[2], ax);
-                ay = fma(wm2[1], col[r + R - 2], ay);
-                ay = fma(wp2[1], col[r + R + 2], ay);
-                az = fma(wm2[2], q[r][R - 2], az);
-                az = fma(wp2[2], q[r][R + 2], az);
+                // fine operator: one FMA chain, the order of fused.cuh's apply13 (same bits)
+                double s = w0 * yc;
+                s = fma(wm1[0], yrow[-1], s);
+                s = fma(wp1[0], yrow[1], s);
+                s = fma(wm2[0], yrow[-2], s);
+                s = fma(wp2[0], yrow[2], s);
+                s = fma(wm1[1], col[r + R - 1], s);
+                s = fma(wp1[1], col[r + R + 1], s);
+                s = fma(wm2[1], col[r + R - 2], s);
+                s = fma(wp2[1], col[r + R + 2], s);
+                s = fma(wm1[2], q[r][R - 1], s);
+                s = fma(wp1[2], q[r][R + 1], s);
+                s = fma(wm2[2], q[r][R - 2], s);
+                s = fma(wp2[2], q[r][R + 2], s);
+                Lv = s;
+            } else {
+                // coarse operator (Alg.2): per-axis partial sums, the order of coarse_persist_kernel
+                double ax = wm1[0] * yrow[-1];
+                ax = fma(wp1[0], yrow[1], ax);
+                double ay = wm1[1] * col[r + R - 1];
+                ay = fma(wp1[1], col[r + R + 1], ay);
+                double az = wm1[2] * q[r][R - 1];
+                az = fma(wp1[2], q[r][R + 1], az);
+                Lv = fma(w0, yc, ax) + (ay + az);
             }
-            const double Lv = fma(w0, yc, ax) + (ay + az);  // right-hand side at this point
 
             if (col_ok && r < rows_ok) {
                 const size_t g = size_t(r) * n;
