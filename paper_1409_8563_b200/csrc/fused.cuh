@@ -56,26 +56,52 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// the same with the barrier's 32-bit shared-window address precomputed by the caller
+// (smem_u32 of a barrier array inside a loop costs an S2R + LEA per use)
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+// a barrier array in shared memory by its 32-bit address
+struct SBars {
+    uint32_t base;
+    __device__ __forceinline__ uint32_t operator[](int i) const { return base + 8u * uint32_t(i); }
+};
 // arrive on the mbarrier once all of this thread's prior cp.async copies land
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
 // add `bytes` of expected transactions to the barrier's current phase (no arrival)
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) { mbar_expect_tx(smem_u32(bar), bytes); }
 // 3-D tensor tile global -> shared on the TMA unit (no L1 data-pipe wavefronts);
 // its bytes complete on the barrier.  map: address of a __grid_constant__ param.
 __device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap *map, int x, int y, int z,
-                                          uint64_t *bar) {
+                                          uint32_t bar) {
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar)
         : "memory");
+}
+__device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap *map, int x, int y, int z,
+                                          uint64_t *bar) {
+    tma_load3(dst, map, x, y, z, smem_u32(bar));
 }
 // Tensor maps of the TMA fills (FusedCfgP::FILL == 2), 3-D (x, y, z) over the
 // n^3 fields, boxes one z plane deep: the padded smem pitch is the box width.
@@ -385,6 +411,8 @@ __device__ __forceinline__ void line_order(int c, int rows, int mid, int hc, int
 template <int KB, class C>
 __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *tm, double *sm,
                                            int items, uint64_t *in_full, uint64_t *in_empty) {
+    const SBars in_full_s{smem_u32(in_full)};
+    const SBars in_empty_s{smem_u32(in_empty)};
     constexpr int DEPTH = C::template DEPTH_K<KB>, EW = C::EWS, IW = C::IWS, TXO = C::TXO;
     constexpr int NP = C::NTP;
     constexpr int NY = (C::Y_CHUNKS + NP - 1) / NP, NU = (C::U_CHUNKS + NP - 1) / NP,
@@ -455,11 +483,11 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
             if constexpr (C::DIAG == 1 || C::DIAG == 2) {
                 if (pos.round() > 0) break;  // only the first fill
             }
-            if (pos.round() > 0) mbar_wait(&in_empty[pos.slot()], (pos.round() - 1) & 1);
+            if (pos.round() > 0) mbar_wait(in_empty_s[pos.slot()], (pos.round() - 1) & 1);
             if constexpr (C::FILL == 2) {
                 if (tma) {
                     if (lane == 0) {
-                        uint64_t *bar = &in_full[pos.slot()];
+                        const uint32_t bar = in_full_s[pos.slot()];
                         const int j = e - 4;
                         const bool ua = KB == K_B && j >= 0 && j < NJ;
                         const bool ca = ua && j >= 2 && j < w.nz + 2;
@@ -474,7 +502,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
                             if (ca) tma_load3(dst + 8 * C::Z_ELEMS, &tm->c, w.x0, w.y0, zaux, bar);
                         }
                     }
-                    cp_async_mbar_arrive(&in_full[pos.slot()]);
+                    cp_async_mbar_arrive(in_full_s[pos.slot()]);
                     zin = (zin + 1 == n) ? 0 : zin + 1;
                     pos.step();
                     continue;
@@ -504,7 +532,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
                     }
                 }
             }
-            cp_async_mbar_arrive(&in_full[pos.slot()]);
+            cp_async_mbar_arrive(in_full_s[pos.slot()]);
             zin = (zin + 1 == n) ? 0 : zin + 1;
             pos.step();
         }
@@ -516,6 +544,10 @@ template <int KB, class C>
 __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int items,
                                           uint64_t *full, uint64_t *empty, uint64_t *in_full,
                                           uint64_t *in_empty, uint32_t tmem) {
+    const SBars full_s{smem_u32(full)};
+    const SBars empty_s{smem_u32(empty)};
+    const SBars in_full_s{smem_u32(in_full)};
+    const SBars in_empty_s{smem_u32(in_empty)};
     constexpr int RPT = C::RPTA, DEPTH = C::template DEPTH_K<KB>, EW = C::EWS, IW = C::IWS, TXO = C::TXO,
                   ZD = C::ZD;
     constexpr int ZS = C::template ZS_ELEMS<KB>;
@@ -572,19 +604,19 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
         RingP<DEPTH> p0 = base;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            if ((C::DIAG != 1 && C::DIAG != 2) || p0.round() == 0) mbar_wait(&in_full[p0.slot()], p0.round() & 1);
+            if ((C::DIAG != 1 && C::DIAG != 2) || p0.round() == 0) mbar_wait(in_full_s[p0.slot()], p0.round() & 1);
             const double *ys = yring + size_t(p0.slot()) * C::Y_ELEMS + sY;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) q[r][e] = lds2(ys + r * IW);
             p0.step();
         }
         // elements 0 and 1 were only needed for the queue
-        mbar_arrive(&in_empty[base.slot()]);
-        mbar_arrive(&in_empty[base.at(1).slot()]);
+        mbar_arrive(in_empty_s[base.slot()]);
+        mbar_arrive(in_empty_s[base.at(1).slot()]);
         RingP<DEPTH> p2 = base.at(2), p4 = p0;  // elements j+2, j+4
         rotating_loop(NJ, [&](auto ph, int j) {
             constexpr int P = decltype(ph)::value;
-            if ((C::DIAG != 1 && C::DIAG != 2) || p4.round() == 0) mbar_wait(&in_full[p4.slot()], p4.round() & 1);  // element j+4 (+ aux j) landed
+            if ((C::DIAG != 1 && C::DIAG != 2) || p4.round() == 0) mbar_wait(in_full_s[p4.slot()], p4.round() & 1);  // element j+4 (+ aux j) landed
             const double *yq = yring + size_t(p4.slot()) * C::Y_ELEMS + sY;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = lds2(yq + r * IW);
@@ -619,7 +651,7 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                     acv[r] = lds2(au + C::Z_ELEMS + (need ? tp0 + r * TXO : 0));
                 }
             }
-            if (C::DIAG != 2 && zpos.round() > 0) mbar_wait(&empty[zpos.slot()], (zpos.round() - 1) & 1);
+            if (C::DIAG != 2 && zpos.round() > 0) mbar_wait(empty_s[zpos.slot()], (zpos.round() - 1) & 1);
             double *zs = zring + size_t(zpos.slot()) * ZS;
             if constexpr (C::TM) {
                 if (tile_lane) {  // intermediate centre, t0 (and u) of this plane -> TMEM
@@ -698,15 +730,15 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                     }
                 }
             }
-            mbar_arrive(&full[zpos.slot()]);
-            mbar_arrive(&in_empty[p2.slot()]);  // element j+2 done (aux j lives in slot j+4)
+            mbar_arrive(full_s[zpos.slot()]);
+            mbar_arrive(in_empty_s[p2.slot()]);  // element j+2 done (aux j lives in slot j+4)
             p2.step();
             p4.step();
             zpos.step();
         });
         // the item's last two input elements were only used by the queue
-        mbar_arrive(&in_empty[p2.slot()]);
-        mbar_arrive(&in_empty[p2.at(1).slot()]);
+        mbar_arrive(in_empty_s[p2.slot()]);
+        mbar_arrive(in_empty_s[p2.at(1).slot()]);
         base = p2.at(2);
     }
 }
@@ -715,6 +747,9 @@ template <int KB, class C>
 __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int items,
                                           uint64_t *full, uint64_t *empty, uint64_t *in_empty,
                                           uint32_t tmem) {
+    const SBars full_s{smem_u32(full)};
+    const SBars empty_s{smem_u32(empty)};
+    const SBars in_empty_s{smem_u32(in_empty)};
     constexpr bool UIN = KB == K_A && C::UIN;
     constexpr int RPT = C::RPT, EW = C::EWS, TXO = C::TXO, ZD = C::ZD, DEPTH = C::template DEPTH_K<KB>;
     constexpr int ZS = C::template ZS_ELEMS<KB>;
@@ -755,7 +790,7 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
         RingP<ZD> zc_pos = zq_pos;  // Z plane j-2 (valid from j = 2)
         rotating_loop(NJ, [&](auto ph, int j) {
             constexpr int P = decltype(ph)::value;
-            if (C::DIAG != 2) mbar_wait(&full[zq_pos.slot()], zq_pos.round() & 1);
+            if (C::DIAG != 2) mbar_wait(full_s[zq_pos.slot()], zq_pos.round() & 1);
             if constexpr (C::TM) {
                 tm_fence_after();
                 TmRaw8 tz;
@@ -817,23 +852,23 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
             }
             if (j >= 2) {
                 if constexpr (C::TM) tm_fence_before();
-                mbar_arrive(&empty[zc_pos.slot()]);
+                mbar_arrive(empty_s[zc_pos.slot()]);
                 zc_pos.step();
             }
             zq_pos.step();
             if constexpr (UIN) {  // input element j: read above (j >= 4) or never (j < 4)
-                mbar_arrive(&in_empty[in_pos.slot()]);
+                mbar_arrive(in_empty_s[in_pos.slot()]);
                 in_pos.step();
             }
         });
         // release the item's last two Z planes (never a centre)
-        mbar_arrive(&empty[zc_pos.slot()]);
+        mbar_arrive(empty_s[zc_pos.slot()]);
         zc_pos.step();
-        mbar_arrive(&empty[zc_pos.slot()]);
+        mbar_arrive(empty_s[zc_pos.slot()]);
         if constexpr (UIN) {  // input elements nz+4 .. nz+7 (z halo only)
 #pragma unroll 1
             for (int e = 0; e < 4; ++e) {
-                mbar_arrive(&in_empty[in_pos.slot()]);
+                mbar_arrive(in_empty_s[in_pos.slot()]);
                 in_pos.step();
             }
         }
@@ -888,6 +923,8 @@ __device__ __forceinline__ void rotating_loop3(int NJ, Body &&body) {
 template <class C>
 __device__ __forceinline__ void stage_c_p(const StencilArgs &a, double *sm, int items,
                                           uint64_t *in_full, uint64_t *in_empty) {
+    const SBars in_full_s{smem_u32(in_full)};
+    const SBars in_empty_s{smem_u32(in_empty)};
     constexpr int RPT = C::RPT, IW = C::IWS, TXO = C::TXO, DEPTH = C::DEPTH;
     const double *yring = sm;
     const int n = a.n;
@@ -922,17 +959,17 @@ __device__ __forceinline__ void stage_c_p(const StencilArgs &a, double *sm, int 
         RingP<DEPTH> p0 = base;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-            mbar_wait(&in_full[p0.slot()], p0.round() & 1);
+            mbar_wait(in_full_s[p0.slot()], p0.round() & 1);
             const double *ys = yring + size_t(p0.slot()) * C::Y_ELEMS + sY;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) q[r][e] = lds2(ys + r * IW);
             p0.step();
         }
-        mbar_arrive(&in_empty[base.slot()]);      // element 0: queue only
+        mbar_arrive(in_empty_s[base.slot()]);      // element 0: queue only
         RingP<DEPTH> pc = base.at(1), pq = p0;  // elements j+1 (centre), j+2
         rotating_loop3(w.nz, [&](auto ph, int j) {
             constexpr int P = decltype(ph)::value;  // q[.][P] = z-1, [P+1] = z, [P+2] = z+1
-            mbar_wait(&in_full[pq.slot()], pq.round() & 1);
+            mbar_wait(in_full_s[pq.slot()], pq.round() & 1);
             const double *yq = yring + size_t(pq.slot()) * C::Y_ELEMS + sY;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) q[r][(P + 2) % 3] = lds2(yq + r * IW);
@@ -969,11 +1006,11 @@ __device__ __forceinline__ void stage_c_p(const StencilArgs &a, double *sm, int 
                 *reinterpret_cast<double2 *>(o0 + size_t(r) * n) = v;
             }
             o0 += nn;
-            mbar_arrive(&in_empty[pc.slot()]);  // the centre plane is no longer read from smem
+            mbar_arrive(in_empty_s[pc.slot()]);  // the centre plane is no longer read from smem
             pc.step();
             pq.step();
         });
-        mbar_arrive(&in_empty[pc.slot()]);  // the item's last element (queue only)
+        mbar_arrive(in_empty_s[pc.slot()]);  // the item's last element (queue only)
         base = pc.at(1);
     }
 }
