@@ -114,7 +114,8 @@ pr_status pr_destroy_grid(pr_grid *grid);
  * bitwise identical: 22 stage B in the stage-A lanes, 23 the stage hand-off
  * through tensor memory, 24 the whole step in ONE kernel (16 B/point), 25 two z
  * planes per warp iteration; PR_WPARAM=1 launches the fused kernels directly
- * with the stage weights as launch parameters instead of CUDA-graph batches.
+ * with the stage weights as launch parameters instead of CUDA-graph batches;
+ * PR_PDL=1 launches them with programmatic dependent launch.
  * Asynchronous on `stream` for device pointers. */
 pr_status pr_fine(pr_grid *grid, const double *u_in, double *u_out, int64_t step0,
                   int64_t n_steps, double dt, void *stream);

@@ -1070,6 +1070,12 @@ fused_persist_kernel(const StencilArgs a, const __grid_constant__ TmaMaps tm) {
     } else {
         __syncthreads();
     }
+    // Programmatic dependent launch (PR_PDL): let the next kernel of the stream be launched
+    // now (its CTAs take an SM as soon as one of ours exits), and wait here until the
+    // previous kernel has completed and its writes are visible -- everything above (barrier
+    // and TMEM set-up) overlaps the previous kernel's tail.  No-ops without the attribute.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int tid = threadIdx.x;
     const bool is_a = C::TM ? (tid < C::NTC || (tid >= C::B_BASE + C::NTB && tid < C::NTA + C::NTB))
                             : tid < C::NTA;

@@ -126,6 +126,7 @@ struct pr_grid {
     int variant = 0;                    // stencil tile variant (PR_TILE env, tuning)
     bool f1 = false;                    // F as ONE kernel per RK4 step (variant 24, NEXT-1)
     bool wparam = false;                // fused F launched directly, weights as parameters
+    bool pdl = false;                   // fused F with programmatic dependent launch (PR_PDL=1)
     bool f2 = false;                    // fused two-kernel RK4 step (tile-aligned n)
     int fvariant = 14;                  // fused tile variant (PR_FTILE env 10..19, tuning)
     bool c2 = false;                    // persistent TMA-fed G kernel (n % 32 == 0; PR_C2=0 disables)
@@ -474,6 +475,21 @@ static void launch_persist(pr_grid *g, const StencilArgs &a, const LaunchCfg &c,
         }
     }
     constexpr auto kern = fused_kernel_of<KB, C>();
+    if (g->pdl) {  // programmatic dependent launch (the kernel waits with griddepcontrol.wait)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(c.blocks);
+        cfg.blockDim = dim3(c.threads);
+        cfg.dynamicSmemBytes = c.smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, kern, a, tm) != cudaSuccess)
+            g->launch_err = fail(PR_ECUDA, "cudaLaunchKernelEx failed (fused kernel %d)", KB);
+        return;
+    }
     kern<<<c.blocks, c.threads, c.smem, st>>>(a, tm);
 }
 
@@ -1031,6 +1047,8 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
         // batches reading the nu table.  Measured neutral at 256^3 / 512^3 and 9 % slower
         // at 128^3 (launch gaps), so the graphs stay the default.
         const char *we = getenv("PR_WPARAM");
+        const char *pe = getenv("PR_PDL");
+        g->pdl = g->f2 && pe && pe[0] == '1';
         g->wparam = g->f2 && !g->f1 && fused_has_wp(g->fvariant) &&
                     (we ? we[0] == '1' : g->fvariant == 25);  // z2 pays its registers with WP
     }
