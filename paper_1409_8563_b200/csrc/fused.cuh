@@ -253,6 +253,7 @@ struct FusedCfgP {
     static constexpr bool COMB = false;  // comb.cuh configs: stage B in the stage-A lanes
     static constexpr bool WP = false;    // weights from the nu table (graph replays)
     static constexpr bool Z2 = false;    // z2.cuh: two z planes per consumer iteration
+    static constexpr bool PF = false;    // stage A loads the next plane's operands one iteration ahead
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = 1, XP = 2,
                          PROD = 1, PW = PW_;  // PW producer warps
     // FILL 0: every plane by 16-byte cp.async; 2: planes of tiles away from the
@@ -325,6 +326,10 @@ using FusedD3 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 0, 3>;  // every tile by T
 // the same kernel with the two stages' weights passed as launch parameters (direct launches):
 // they sit in uniform registers / the constant bank instead of 26 registers per thread
 template <class C> struct WithWP : C { static constexpr bool WP = true; };
+// stage A software-pipelined: the next plane's shared-memory operands are loaded before
+// this plane's stencil, so their latency hides under its FMA chains (more live registers)
+template <class C> struct WithPF : C { static constexpr bool PF = true; };
+using FusedPF = WithPF<FusedP4>;  // PR_FTILE=29 (PRK_VARIANTS): 12 % slower, spills at 168 registers
 #ifdef PRK_VARIANTS  // tuning history (profiles/r01_kernel_bench_variants.txt)
 using FusedP0 = FusedCfgP<16, 7, 4, 2, 2, 1>;   // one producer warp
 using FusedP1 = FusedCfgP<16, 9, 4, 2, 2, 1>;
@@ -614,43 +619,65 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
         mbar_arrive(in_empty_s[base.slot()]);
         mbar_arrive(in_empty_s[base.at(1).slot()]);
         RingP<DEPTH> p2 = base.at(2), p4 = p0;  // elements j+2, j+4
+        // the shared-memory operands of one plane: the new z-queue entry (element j+4), the
+        // y (+-2 rows) and x neighbours on element j+2, K_B's u and acc (aux j)
+        struct LdA {
+            double2 qn[RPT], ym[2], yp[2], L[RPT], R[RPT], ub[KB == K_B ? RPT : 1], ac[KB == K_B ? RPT : 1];
+        };
+        auto load = [&](LdA &d, RingP<DEPTH> e4, RingP<DEPTH> e2) {
+            if ((C::DIAG != 1 && C::DIAG != 2) || e4.round() == 0) mbar_wait(in_full_s[e4.slot()], e4.round() & 1);  // element j+4 (+ aux j) landed
+            const double *yq = yring + size_t(e4.slot()) * C::Y_ELEMS + sY;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) d.qn[r] = lds2(yq + r * IW);
+            const double *ys = yring + size_t(e2.slot()) * C::Y_ELEMS + sY;
+            d.ym[0] = lds2(ys - 2 * IW);
+            d.ym[1] = lds2(ys - IW);
+            d.yp[0] = lds2(ys + RPT * IW);
+            d.yp[1] = lds2(ys + (RPT + 1) * IW);
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                d.L[r] = lds2(ys + r * IW - 2);
+                d.R[r] = lds2(ys + r * IW + 2);
+            }
+        };
+        // K_B: u on the ring and the acc values of this lane's tile points (lanes without a
+        // tile point read entry 0); aux j rides with element j+4 (waited for in load)
+        auto load_aux = [&](LdA &d, RingP<DEPTH> e4) {
+            if constexpr (KB == K_B) {
+                const double *au = aring + size_t(e4.slot()) * C::AUX_ELEMS;  // aux j
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {
+                    d.ub[r] = lds2(au + sZ + r * EW);
+                    const int er = r0 + r;
+                    const bool need = tcol && er >= 2 && er < C::TYO + 2;
+                    d.ac[r] = lds2(au + C::Z_ELEMS + (need ? tp0 + r * TXO : 0));
+                }
+            }
+        };
+        [[maybe_unused]] LdA nx;  // PF: the next plane's operands, loaded one iteration ahead
+        if constexpr (C::PF) load(nx, p4, p2);
         rotating_loop(NJ, [&](auto ph, int j) {
             constexpr int P = decltype(ph)::value;
-            if ((C::DIAG != 1 && C::DIAG != 2) || p4.round() == 0) mbar_wait(in_full_s[p4.slot()], p4.round() & 1);  // element j+4 (+ aux j) landed
-            const double *yq = yring + size_t(p4.slot()) * C::Y_ELEMS + sY;
+            LdA cur;
+            if constexpr (C::PF) {
+                cur = nx;
+                if (j + 1 < NJ) load(nx, p4.at(1), p2.at(1));
+            } else {
+                load(cur, p4, p2);
+            }
+            load_aux(cur, p4);
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = lds2(yq + r * IW);
-            const double *ys = yring + size_t(p2.slot()) * C::Y_ELEMS + sY;
+            for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = cur.qn[r];
             double2 col[RPT + 4];
 #pragma unroll
             for (int r = 0; r < RPT + 4; ++r)
-                col[r] = (r >= 2 && r < RPT + 2) ? q[r - 2][(P + 2) % 5] : lds2(ys + (r - 2) * IW);
-            // K_B: u on the ring is in shared memory already; load it before the
-            // stencil so its latency hides under the FMAs
-            const double *au = aring + size_t(p4.slot()) * C::AUX_ELEMS;  // aux j
+                col[r] = r < 2 ? cur.ym[r] : r < RPT + 2 ? q[r - 2][(P + 2) % 5] : cur.yp[r - RPT - 2];
             [[maybe_unused]] const bool outp = j >= 2 && j < w.nz + 2;
-            double2 ubv[KB == K_B ? RPT : 1];
-            if constexpr (KB == K_B) {
-#pragma unroll
-                for (int r = 0; r < RPT; ++r) ubv[r] = lds2(au + sZ + r * EW);
-            } else {
-                (void)au;
-            }
+            const double2 *ubv = cur.ub, *acv = cur.ac;
             double2 k[RPT];
 #pragma unroll
             for (int r = 0; r < RPT; ++r)
-                k[r] = apply_pair<P>(W, lds2(ys + r * IW - 2), lds2(ys + r * IW + 2), col[r],
-                                     col[r + 1], col[r + 3], col[r + 4], q[r]);
-            // K_B: the acc values of this lane's tile points, read before the ring wait
-            double2 acv[KB == K_B ? RPT : 1];
-            if constexpr (KB == K_B) {
-#pragma unroll
-                for (int r = 0; r < RPT; ++r) {  // lanes without a tile point read entry 0
-                    const int er = r0 + r;
-                    const bool need = tcol && er >= 2 && er < C::TYO + 2;
-                    acv[r] = lds2(au + C::Z_ELEMS + (need ? tp0 + r * TXO : 0));
-                }
-            }
+                k[r] = apply_pair<P>(W, cur.L[r], cur.R[r], col[r], col[r + 1], col[r + 3], col[r + 4], q[r]);
             if (C::DIAG != 2 && zpos.round() > 0) mbar_wait(empty_s[zpos.slot()], (zpos.round() - 1) & 1);
             double *zs = zring + size_t(zpos.slot()) * ZS;
             if constexpr (C::TM) {
