@@ -70,6 +70,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// non-blocking probe of the phase with the given parity (1 = completed); acquire on success.
+// Issued well ahead of its use, its latency overlaps independent work (try_wait costs ~90
+// cycles even on a completed phase, B300_MICROARCH.md "mbarrier")
+__device__ __forceinline__ uint32_t mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok;
+}
 __device__ __forceinline__ void cp_async_mbar_arrive(uint32_t bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -254,6 +268,7 @@ struct FusedCfgP {
     static constexpr bool WP = false;    // weights from the nu table (graph replays)
     static constexpr bool Z2 = false;    // z2.cuh: two z planes per consumer iteration
     static constexpr bool PF = false;    // stage A loads the next plane's operands one iteration ahead
+    static constexpr bool SW = false;    // split-phase ring waits: probe early, block only on failure
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = 1, XP = 2,
                          PROD = 1, PW = PW_;  // PW producer warps
     // FILL 0: every plane by 16-byte cp.async; 2: planes of tiles away from the
@@ -329,8 +344,15 @@ template <class C> struct WithWP : C { static constexpr bool WP = true; };
 // stage A software-pipelined: the next plane's shared-memory operands are loaded before
 // this plane's stencil, so their latency hides under its FMA chains (more live registers)
 template <class C> struct WithPF : C { static constexpr bool PF = true; };
+// split-phase ring waits: each consumer probes (mbarrier.test_wait) the barrier it needs
+// next one step ahead and blocks (try_wait) only if the probe failed
+template <class C> struct WithSW : C { static constexpr bool SW = true; };
+using FusedSW = WithSW<FusedP4>;
 using FusedPF = WithPF<FusedP4>;  // PR_FTILE=29 (PRK_VARIANTS): 12 % slower, spills at 168 registers
 #ifdef PRK_VARIANTS  // tuning history (profiles/r01_kernel_bench_variants.txt)
+// deeper intermediate (Z) rings: stage A may run further ahead of stage B (K_A ZD 6 / 8, K_B 5)
+using FusedZD6 = FusedCfgP<16, 9, 6, 2, 2, 2, 2>;
+using FusedZD8 = FusedCfgP<16, 9, 8, 2, 2, 2, 2>;
 using FusedP0 = FusedCfgP<16, 7, 4, 2, 2, 1>;   // one producer warp
 using FusedP1 = FusedCfgP<16, 9, 4, 2, 2, 1>;
 using FusedP2 = FusedCfgP<16, 8, 5, 2, 2, 2>;   // 5-slot intermediate ring
@@ -624,8 +646,9 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
         struct LdA {
             double2 qn[RPT], ym[2], yp[2], L[RPT], R[RPT], ub[KB == K_B ? RPT : 1], ac[KB == K_B ? RPT : 1];
         };
-        auto load = [&](LdA &d, RingP<DEPTH> e4, RingP<DEPTH> e2) {
-            if ((C::DIAG != 1 && C::DIAG != 2) || e4.round() == 0) mbar_wait(in_full_s[e4.slot()], e4.round() & 1);  // element j+4 (+ aux j) landed
+        auto load = [&](LdA &d, RingP<DEPTH> e4, RingP<DEPTH> e2, bool ready = false) {
+            if (!ready && ((C::DIAG != 1 && C::DIAG != 2) || e4.round() == 0))
+                mbar_wait(in_full_s[e4.slot()], e4.round() & 1);  // element j+4 (+ aux j) landed
             const double *yq = yring + size_t(e4.slot()) * C::Y_ELEMS + sY;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) d.qn[r] = lds2(yq + r * IW);
@@ -656,6 +679,7 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
         };
         [[maybe_unused]] LdA nx;  // PF: the next plane's operands, loaded one iteration ahead
         if constexpr (C::PF) load(nx, p4, p2);
+        uint32_t in_ok = 0;  // SW: element j+4 already probed complete
         rotating_loop(NJ, [&](auto ph, int j) {
             constexpr int P = decltype(ph)::value;
             LdA cur;
@@ -663,9 +687,18 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                 cur = nx;
                 if (j + 1 < NJ) load(nx, p4.at(1), p2.at(1));
             } else {
-                load(cur, p4, p2);
+                load(cur, p4, p2, C::SW && in_ok);
             }
             load_aux(cur, p4);
+            [[maybe_unused]] uint32_t z_ok = 0;
+            if constexpr (C::SW) {  // probes for the next element and this plane's Z slot
+                // branch-free, so that the stencil below shares their basic block: the probe of
+                // element j+5 may look at the next item's first slot (harmless, masked), the
+                // round-0 probe of a Z slot (parity 1 on a fresh barrier) passes at once
+                const RingP<DEPTH> e5 = p4.at(1);
+                in_ok = mbar_test(in_full_s[e5.slot()], e5.round() & 1) & uint32_t(j + 1 < NJ);
+                z_ok = mbar_test(empty_s[zpos.slot()], uint32_t(zpos.round() - 1) & 1);
+            }
 #pragma unroll
             for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = cur.qn[r];
             double2 col[RPT + 4];
@@ -678,7 +711,8 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
 #pragma unroll
             for (int r = 0; r < RPT; ++r)
                 k[r] = apply_pair<P>(W, cur.L[r], cur.R[r], col[r], col[r + 1], col[r + 3], col[r + 4], q[r]);
-            if (C::DIAG != 2 && zpos.round() > 0) mbar_wait(empty_s[zpos.slot()], (zpos.round() - 1) & 1);
+            if (C::DIAG != 2 && zpos.round() > 0 && !(C::SW && z_ok))
+                mbar_wait(empty_s[zpos.slot()], (zpos.round() - 1) & 1);
             double *zs = zring + size_t(zpos.slot()) * ZS;
             if constexpr (C::TM) {
                 if (tile_lane) {  // intermediate centre, t0 (and u) of this plane -> TMEM
@@ -806,6 +840,7 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
 
     RingP<ZD> zq_pos;     // Z plane j of the current item
     RingP<DEPTH> in_pos;  // UIN: input element j of the current item
+    [[maybe_unused]] uint32_t full_ok = 0;  // SW: Z plane j already probed complete
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const WorkItem w = decode_item(a, item, TXO, C::TYO);
@@ -817,7 +852,7 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
         RingP<ZD> zc_pos = zq_pos;  // Z plane j-2 (valid from j = 2)
         rotating_loop(NJ, [&](auto ph, int j) {
             constexpr int P = decltype(ph)::value;
-            if (C::DIAG != 2) mbar_wait(full_s[zq_pos.slot()], zq_pos.round() & 1);
+            if (C::DIAG != 2 && !(C::SW && full_ok)) mbar_wait(full_s[zq_pos.slot()], zq_pos.round() & 1);
             if constexpr (C::TM) {
                 tm_fence_after();
                 TmRaw8 tz;
@@ -829,6 +864,10 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
                 const double *zq = zring + size_t(zq_pos.slot()) * ZS + sZ;
 #pragma unroll
                 for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = lds2(zq + r * EW);
+            }
+            if constexpr (C::SW) {  // probe plane j+1 (possibly the next item's first plane)
+                const RingP<ZD> zn = zq_pos.at(1);
+                full_ok = mbar_test(full_s[zn.slot()], zn.round() & 1);
             }
             if (j >= 4 && valid) {
                 const double *zs = zring + size_t(zc_pos.slot()) * ZS;
