@@ -32,6 +32,7 @@ template <int TYO_, int DEPTH_, int PW_ = 2, int FILL_ = 2, int ZD_ = 4>
 struct CombCfg {
     static constexpr bool COMB = true, Z2 = false, WP = false;
     static constexpr int DIAG = 0;
+    static constexpr bool PIN = false;
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, PW = PW_, FILL = FILL_;
     static constexpr int RPT = 2, RPTA = 2, XP = 2;
     static constexpr int EW = TXO + 4, EH = TYO + 4, IW = TXO + 8, IH = TYO + 8;

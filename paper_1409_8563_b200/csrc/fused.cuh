@@ -92,6 +92,25 @@ struct SBars {
     uint32_t base;
     __device__ __forceinline__ uint32_t operator[](int i) const { return base + 8u * uint32_t(i); }
 };
+// a value the compiler cannot rematerialise: kept in a register instead of being rebuilt
+// (S2R SR_CgaCtaId + LEA for a shared-window address) in every loop iteration
+__device__ __forceinline__ uint32_t pin_u32(uint32_t v) {
+    uint32_t r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+// the dynamic shared-memory base with its window address pinned the same way (the generic
+// pointer is rebuilt from the shared address, so loads through it stay LDS)
+template <class C> __device__ __forceinline__ double *smem_base(double *sm) {
+    if constexpr (C::PIN) {
+        return reinterpret_cast<double *>(__cvta_shared_to_generic(pin_u32(smem_u32(sm))));
+    } else {
+        return sm;
+    }
+}
+template <class C> __device__ __forceinline__ SBars sbars(const uint64_t *bar) {
+    return SBars{C::PIN ? pin_u32(smem_u32(bar)) : smem_u32(bar)};
+}
 // arrive on the mbarrier once all of this thread's prior cp.async copies land
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
@@ -269,6 +288,9 @@ struct FusedCfgP {
     static constexpr bool Z2 = false;    // z2.cuh: two z planes per consumer iteration
     static constexpr bool PF = false;    // stage A loads the next plane's operands one iteration ahead
     static constexpr bool SW = false;    // split-phase ring waits: probe early, block only on failure
+    // shared-window addresses of the barriers and rings pinned in registers (pin_u32):
+    // 2-3 % faster than letting the compiler rebuild them per iteration (variant 36 = off)
+    static constexpr bool PIN = true;
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = 1, XP = 2,
                          PROD = 1, PW = PW_;  // PW producer warps
     // FILL 0: every plane by 16-byte cp.async; 2: planes of tiles away from the
@@ -348,6 +370,8 @@ template <class C> struct WithPF : C { static constexpr bool PF = true; };
 // next one step ahead and blocks (try_wait) only if the probe failed
 template <class C> struct WithSW : C { static constexpr bool SW = true; };
 using FusedSW = WithSW<FusedP4>;
+template <class C> struct NoPIN : C { static constexpr bool PIN = false; };
+using FusedNoPIN = NoPIN<FusedP4>;
 using FusedPF = WithPF<FusedP4>;  // PR_FTILE=29 (PRK_VARIANTS): 12 % slower, spills at 168 registers
 #ifdef PRK_VARIANTS  // tuning history (profiles/r01_kernel_bench_variants.txt)
 // deeper intermediate (Z) rings: stage A may run further ahead of stage B (K_A ZD 6 / 8, K_B 5)
@@ -438,8 +462,8 @@ __device__ __forceinline__ void line_order(int c, int rows, int mid, int hc, int
 template <int KB, class C>
 __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *tm, double *sm,
                                            int items, uint64_t *in_full, uint64_t *in_empty) {
-    const SBars in_full_s{smem_u32(in_full)};
-    const SBars in_empty_s{smem_u32(in_empty)};
+    const SBars in_full_s = sbars<C>(in_full);
+    const SBars in_empty_s = sbars<C>(in_empty);
     constexpr int DEPTH = C::template DEPTH_K<KB>, EW = C::EWS, IW = C::IWS, TXO = C::TXO;
     constexpr int NP = C::NTP;
     constexpr int NY = (C::Y_CHUNKS + NP - 1) / NP, NU = (C::U_CHUNKS + NP - 1) / NP,
@@ -571,14 +595,14 @@ template <int KB, class C>
 __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int items,
                                           uint64_t *full, uint64_t *empty, uint64_t *in_full,
                                           uint64_t *in_empty, uint32_t tmem) {
-    const SBars full_s{smem_u32(full)};
-    const SBars empty_s{smem_u32(empty)};
-    const SBars in_full_s{smem_u32(in_full)};
-    const SBars in_empty_s{smem_u32(in_empty)};
+    const SBars full_s = sbars<C>(full);
+    const SBars empty_s = sbars<C>(empty);
+    const SBars in_full_s = sbars<C>(in_full);
+    const SBars in_empty_s = sbars<C>(in_empty);
     constexpr int RPT = C::RPTA, DEPTH = C::template DEPTH_K<KB>, EW = C::EWS, IW = C::IWS, TXO = C::TXO,
                   ZD = C::ZD;
     constexpr int ZS = C::template ZS_ELEMS<KB>;
-    double *yring = sm;
+    double *yring = smem_base<C>(sm);
     double *aring = yring + size_t(DEPTH) * C::Y_ELEMS;
     double *zring = aring + (KB == K_B ? size_t(C::AD) * C::AUX_ELEMS : 0);
     // stage-A lane index: TM puts the tile lanes first (threads 0 .. NTC-1) and the ring
@@ -808,12 +832,13 @@ template <int KB, class C>
 __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int items,
                                           uint64_t *full, uint64_t *empty, uint64_t *in_empty,
                                           uint32_t tmem) {
-    const SBars full_s{smem_u32(full)};
-    const SBars empty_s{smem_u32(empty)};
-    const SBars in_empty_s{smem_u32(in_empty)};
+    const SBars full_s = sbars<C>(full);
+    const SBars empty_s = sbars<C>(empty);
+    const SBars in_empty_s = sbars<C>(in_empty);
     constexpr bool UIN = KB == K_A && C::UIN;
     constexpr int RPT = C::RPT, EW = C::EWS, TXO = C::TXO, ZD = C::ZD, DEPTH = C::template DEPTH_K<KB>;
     constexpr int ZS = C::template ZS_ELEMS<KB>;
+    sm = smem_base<C>(sm);
     double *zring = sm + size_t(DEPTH) * C::Y_ELEMS + (KB == K_B ? size_t(C::AD) * C::AUX_ELEMS : 0);
     const int n = a.n;
     const size_t nn = size_t(n) * n;
@@ -952,6 +977,7 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
 template <int TYO_, int DEPTH_, int RPT_, int PW_, int FILL_>
 struct CoarseCfgP {
     static constexpr int DIAG = 0;
+    static constexpr bool PIN = false;
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, RPT = RPT_, PW = PW_, FILL = FILL_;
     static constexpr int HX = 2, HY = 1, HZ = 1;  // radius-1 stencil; x halo pair-aligned
     static constexpr int IW = TXO + 2 * HX, IH = TYO + 2 * HY, IWS = IW;
@@ -989,8 +1015,8 @@ __device__ __forceinline__ void rotating_loop3(int NJ, Body &&body) {
 template <class C>
 __device__ __forceinline__ void stage_c_p(const StencilArgs &a, double *sm, int items,
                                           uint64_t *in_full, uint64_t *in_empty) {
-    const SBars in_full_s{smem_u32(in_full)};
-    const SBars in_empty_s{smem_u32(in_empty)};
+    const SBars in_full_s = sbars<C>(in_full);
+    const SBars in_empty_s = sbars<C>(in_empty);
     constexpr int RPT = C::RPT, IW = C::IWS, TXO = C::TXO, DEPTH = C::DEPTH;
     const double *yring = sm;
     const int n = a.n;
