@@ -291,6 +291,7 @@ struct FusedCfgP {
     // shared-window addresses of the barriers and rings pinned in registers (pin_u32):
     // 2-3 % faster than letting the compiler rebuild them per iteration (variant 36 = off)
     static constexpr bool PIN = true;
+    static constexpr bool OFF32 = false;  // stage-B stores by 32-bit element offsets (n^3 < 2^32)
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = 1, XP = 2,
                          PROD = 1, PW = PW_;  // PW producer warps
     // FILL 0: every plane by 16-byte cp.async; 2: planes of tiles away from the
@@ -372,6 +373,8 @@ template <class C> struct WithSW : C { static constexpr bool SW = true; };
 using FusedSW = WithSW<FusedP4>;
 template <class C> struct NoPIN : C { static constexpr bool PIN = false; };
 using FusedNoPIN = NoPIN<FusedP4>;
+template <class C> struct WithOFF32 : C { static constexpr bool OFF32 = true; };
+using FusedOFF32 = WithOFF32<FusedP4>;
 using FusedPF = WithPF<FusedP4>;  // PR_FTILE=29 (PRK_VARIANTS): 12 % slower, spills at 168 registers
 #ifdef PRK_VARIANTS  // tuning history (profiles/r01_kernel_bench_variants.txt)
 // deeper intermediate (Z) rings: stage A may run further ahead of stage B (K_A ZD 6 / 8, K_B 5)
@@ -870,6 +873,10 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const WorkItem w = decode_item(a, item, TXO, C::TYO);
         const int NJ = w.nz + 4;
+        // OFF32: one 32-bit element offset for both outputs (n^3 < 2^32), each store address a
+        // single IMAD.WIDE off the kernel-parameter base instead of 64-bit pointer pairs
+        [[maybe_unused]] uint32_t off = uint32_t(w.z_begin) * uint32_t(nn) + uint32_t(w.y0 + r0) * uint32_t(n) +
+                                        uint32_t(w.x0 + 2 * m);
         double *o0 = a.o0 + size_t(w.z_begin) * nn + size_t(w.y0 + r0) * n + w.x0 + 2 * m;
         double *o1 = KB == K_A ? a.o1 + size_t(w.z_begin) * nn + size_t(w.y0 + r0) * n + w.x0 + 2 * m
                                : nullptr;
@@ -927,19 +934,33 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
                         double2 v0, v1;
                         v0.x = t0.x + (dt / 3.0) * kB.x;  v0.y = t0.y + (dt / 3.0) * kB.y;
                         v1.x = t1.x + (dt / 2.0) * kB.x;  v1.y = t1.y + (dt / 2.0) * kB.y;
-                        *reinterpret_cast<double2 *>(o0 + gofs) = v0;
-                        *reinterpret_cast<double2 *>(o1 + gofs) = v1;
+                        if constexpr (C::OFF32) {
+                            const uint32_t e = off + uint32_t(r) * uint32_t(n);
+                            *reinterpret_cast<double2 *>(a.o0 + e) = v0;
+                            *reinterpret_cast<double2 *>(a.o1 + e) = v1;
+                        } else {
+                            *reinterpret_cast<double2 *>(o0 + gofs) = v0;
+                            *reinterpret_cast<double2 *>(o1 + gofs) = v1;
+                        }
                     } else {
                         const double2 t0 = C::TM ? tm_row(tt0, r) : lds2(zs + C::Z_ELEMS + sT + r * TXO);
                         double2 v0;
                         v0.x = t0.x + (dt / 6.0) * kB.x;  v0.y = t0.y + (dt / 6.0) * kB.y;
-                        *reinterpret_cast<double2 *>(o0 + gofs) = v0;
+                        if constexpr (C::OFF32) {
+                            *reinterpret_cast<double2 *>(a.o0 + (off + uint32_t(r) * uint32_t(n))) = v0;
+                        } else {
+                            *reinterpret_cast<double2 *>(o0 + gofs) = v0;
+                        }
                     }
                 }
             }
             if (j >= 4) {
-                o0 += nn;
-                if (KB == K_A) o1 += nn;
+                if constexpr (C::OFF32) {
+                    off += uint32_t(nn);
+                } else {
+                    o0 += nn;
+                    if (KB == K_A) o1 += nn;
+                }
             }
             if (j >= 2) {
                 if constexpr (C::TM) tm_fence_before();
