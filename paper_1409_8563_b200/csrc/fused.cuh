@@ -477,7 +477,8 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
     const size_t nn = size_t(n) * n;
     // 0 .. NP-1 (NTA + NTB is a multiple of 32, so the % keeps the range visible)
     const int lane = (threadIdx.x - (C::NTA + C::NTB)) % NP;
-    const uint32_t yring_s = smem_u32(yring), aring_s = smem_u32(aring);
+    const uint32_t yring_s = C::PIN ? pin_u32(smem_u32(yring)) : smem_u32(yring);
+    const uint32_t aring_s = yring_s + uint32_t(sizeof(double) * DEPTH * C::Y_ELEMS);
     RingP<DEPTH> pos;
 #pragma unroll 1
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
