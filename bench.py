@@ -197,7 +197,7 @@ def workload_config(cfg, world, Np, K, args):
                   "fields L2-resident"}
 
 
-def run_reference(args, cfg):
+def run_reference(args, cfg, out):
     """--impl reference: the oracle (oracle/oracle.c, as it stands) timed on the host
     cores, rank 0 only.  Each bench step is ONE multi-step orc_fine call: a bounded
     sample of the workload's serial fine solve, sized so the run ends in minutes."""
@@ -236,7 +236,7 @@ def run_reference(args, cfg):
                              "sample": f"each step = one orc_fine call of {S} serial fine RK4 steps of "
                                        f"the {cfg.name} grid ({n}^3), {oracle.threads()} OpenMP threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(out, line)
     return 0
 
 
@@ -271,7 +271,23 @@ def modal_parity(cfg, Np, K, uT, defects, flags_g_mesh):
             "reference": "exact discrete Fourier-mode recurrence of the same Alg.1 run (tests/modal_ref.py)"}
 
 
+def claim_stdout():
+    """Keep the process's stdout for the one JSON line: from here on fd 1 points at stderr,
+    so banners printed by libraries (NCCL's version line under torchrun, ...) cannot precede
+    or interleave with it.  Returns a writer on the original stdout."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    return os.fdopen(saved, "w")
+
+
+def emit(out, line):
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    out = claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -306,7 +322,7 @@ def main():
         cfg = cfg.with_(Nt=args.Nt or cfg.Nt, NC=args.NC or cfg.NC,
                         name=f"{cfg.name}[Nt={args.Nt or cfg.Nt},NC={args.NC or cfg.NC}]")
     if args.impl == "reference":
-        return run_reference(args, cfg)
+        return run_reference(args, cfg, out)
 
     import torch
     import torch.distributed as dist
@@ -565,7 +581,7 @@ def main():
             line["e2e"] = e2e
         if cpu:
             line["cpu_baseline"] = cpu
-        print(json.dumps(line), flush=True)
+        emit(out, line)
     grid.destroy()
     if world > 1:
         dist.barrier(device_ids=[local])
