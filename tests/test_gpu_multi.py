@@ -49,6 +49,25 @@ def test_parareal_multi_gpu(W, n, Np, K, tol, handoff):
     assert info["ok"] and info["bitwise_equal_to_1gpu"], info
 
 
+@pytest.mark.parametrize("handoff", ["nccl", "peer"])
+@pytest.mark.parametrize("W,K", [(2, 1000), (4, 350)])
+def test_multi_gpu_handoff_stress(W, K, handoff):
+    """~10^3 hand-offs between processes on different GPUs (n = 32, N_p = W, K iterations on
+    a 64-step horizon, two calls): u_T and every d^k bitwise equal to the one-GPU run of the
+    same slices, so the NCCL and the peer-store paths agree with each other bit for bit."""
+    if ngpus() < W:
+        pytest.skip(f"needs {W} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={W}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "tools", "mgpu_check.py"), "32", str(W), str(K), "0", handoff, "stress"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert res.returncode == 0 and lines, res.stdout[-3000:] + res.stderr[-3000:]
+    info = json.loads(lines[-1])
+    assert info["ok"] and info["bitwise_equal_to_1gpu"] and info["repeat_equal"], \
+        {k: info[k] for k in info if k != "defects"}
+
+
 @pytest.mark.parametrize("handoff", ["nccl"])
 def test_stuck_predecessor_nccl(handoff):
     """Rank 0 never sends: rank 1's pr_parareal returns PR_ENCCL with its rank and

@@ -1,6 +1,6 @@
 """Multi-GPU Parareal check (run under torchrun, one process per GPU).
 
-    torchrun --nproc-per-node W --master-addr 127.0.0.1 --master-port P tools/mgpu_check.py [n] [Np] [K] [tol] [nccl|peer]
+    torchrun --nproc-per-node W --master-addr 127.0.0.1 --master-port P tools/mgpu_check.py [n] [Np] [K] [tol] [nccl|peer] [stress]
 
 Every rank runs pr_parareal on its slice group with NCCL hand-off; the last
 rank compares u_T and d^k with (a) a single-GPU run of the same N_p slices
@@ -37,6 +37,9 @@ def main():
     T, Nt, NC = 0.1, 2048 * (n // 32) ** 2 if n <= 64 else 2048, 128 * (n // 32) ** 2 if n <= 64 else 128
     if n > 64:  # short horizon with the cfg-style step sizes
         T, Nt, NC = 0.1 / 64, 2 ** 11, 2 ** 7
+    stress = len(sys.argv) > 6 and sys.argv[6] == "stress"
+    if stress:  # many hand-offs: the default step sizes on a 64-step horizon, K up to ~10^3
+        T, Nt, NC = 0.1 * 64 / 2048, 64, 8
     world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -82,7 +85,7 @@ def main():
         info["bitwise_equal_to_1gpu"] = bool(torch.equal(uT, uT1)) and d1 == d
         ok &= info["bitwise_equal_to_1gpu"] and same(d2, d)
         # (b) oracle (small grids only)
-        if n <= 48:
+        if n <= 48 and not stress:  # (stress: K ~ 10^3 iterations, bitwise vs (a) only)
             import oracle
             p = oracle.Problem(n, T=T)
             o0 = oracle.initial(n)
