@@ -1874,7 +1874,11 @@ pr_status pr_parareal(pr_grid *g, const pr_parareal_cfg *cfg, const double *u0, 
                 recvd = true;
                 break;
             }
-            // the receive buffer was last read by F of iteration k-1 (done: stream order)
+            // the receive buffer was last read by F of iteration k-1, but the receive is posted
+            // only after THIS iteration's F: NCCL's receive kernel holds an SM while it waits for
+            // the data, and one of F's persistent CTAs (one per SM, statically assigned work)
+            // would then wait for that SM -- posting it after iteration k-1 instead made the
+            // 4-GPU NCCL solve 18 % slower (profiles/r02_gpu_multi_w4_nccl_recv.log)
             CK(cudaStreamWaitEvent(g->comm_stream, fdone_ev, 0));
             NCK(ncclRecv(recvb, msg, ncclDouble, op.peer, g->comm, g->comm_stream), op.k);
             CK(cudaEventRecord(recv_ev(op.k), g->comm_stream));
