@@ -109,11 +109,11 @@ pr_status pr_destroy_grid(pr_grid *grid);
  * allowed; any other overlap is PR_EINVAL.  n_steps = 0 copies.  One step is
  * two fused kernels (stages 1+2 and 3+4, 56 B/point) when n is a multiple of
  * 32, else four fused stage passes (128 B/point); both give bitwise identical
- * results.  The environment variable PR_FTILE (read at
- * pr_create_grid) selects an alternative design of the two-kernel step, all
- * bitwise identical: 22 stage B in the stage-A lanes, 23 the stage hand-off
- * through tensor memory, 24 the whole step in ONE kernel (16 B/point), 25 two z
- * planes per warp iteration; PR_WPARAM=1 launches the fused kernels directly
+ * results.  Default two-kernel design: the per-point stage hand-off
+ * through tensor memory (23) for n >= 256, through shared memory (14) below.  The
+ * environment variable PR_FTILE (read at pr_create_grid) selects another design,
+ * all bitwise identical: 14 or 23 at any n, 22 stage B in the stage-A lanes, 24
+ * the whole step in ONE kernel (16 B/point), 25 two z planes per warp iteration; PR_WPARAM=1 launches the fused kernels directly
  * with the stage weights as launch parameters instead of CUDA-graph batches;
  * PR_PDL=1 launches them with programmatic dependent launch.
  * Asynchronous on `stream` for device pointers. */

@@ -128,7 +128,7 @@ struct pr_grid {
     bool wparam = false;                // fused F launched directly, weights as parameters
     bool pdl = false;                   // fused F with programmatic dependent launch (PR_PDL=1)
     bool f2 = false;                    // fused two-kernel RK4 step (tile-aligned n)
-    int fvariant = 14;                  // fused tile variant (PR_FTILE env 10..19, tuning)
+    int fvariant = 14;                  // fused F variant (PR_FTILE; default set per n below)
     bool c2 = false;                    // persistent TMA-fed G kernel (n % 32 == 0; PR_C2=0 disables)
     int cvariant = 0;                   // its variant (PR_CTILE 0..2)
     LaunchCfg lcp;                      // its launch config
@@ -1037,6 +1037,10 @@ pr_status pr_create_grid(const pr_problem *problem, int32_t cuda_device, pr_grid
     if ((s = setup_kind<K_S4>(g)) != PR_OK) return bail(s);
     {
         const char *fe = getenv("PR_F2");
+        // default: the TMEM stage-A -> stage-B hand-off (23) from 256^3 up, where it is 2-4 %
+        // faster than the shared-memory hand-off (14; bench 2019 vs 2061 ms per solve), 14
+        // below (3 % faster at 128^3); both give the same bits (test_fused_variants_bitwise)
+        g->fvariant = n >= 256 ? 23 : 14;
         if (const char *fv = getenv("PR_FTILE")) g->fvariant = atoi(fv);
         int tya = 0, tyb = 0;
         fused_tiles(g->fvariant, &tya, &tyb);

@@ -1,8 +1,8 @@
 """The built library contains the Blackwell instructions DESIGN.md claims (CPU test:
 cuobjdump -sass of libparareal.so): TMA tensor loads (UTMALDG) and mbarrier ops (SYNCS)
-in the default persistent F and G kernels; tcgen05.ld / tcgen05.st (LDTM / STTM) and
-tcgen05.alloc in the TMEM hand-off kernels (PR_FTILE=23); no legacy tensor-core or
-Hopper instructions anywhere (HMMA, HGMMA)."""
+in the persistent F and G kernels; tcgen05.ld / tcgen05.st (LDTM / STTM) and
+tcgen05.alloc in the TMEM hand-off kernels (PR_FTILE=23, the default F for n >= 256); no
+legacy tensor-core or Hopper instructions anywhere (HMMA, HGMMA)."""
 import os
 import shutil
 import sys
@@ -28,7 +28,7 @@ def kernels(mix, *parts):
 
 
 def test_default_kernels_use_tma_and_mbarriers(mix):
-    default = kernels(mix, "fused_persist_kernel", "ELi9ELi0ELi0EE")  # variant 14 (TM = 0)
+    default = kernels(mix, "fused_persist_kernel", "ELi9ELi0ELi0EE")  # variant 14 (n < 256)
     assert len(default) >= 2
     for f, c in default.items():
         assert c["UTMALDG"] >= 1 and c["SYNCS"] >= 10 and c["DFMA"] > 500, f
@@ -37,10 +37,11 @@ def test_default_kernels_use_tma_and_mbarriers(mix):
 
 
 def test_tmem_variant_uses_tcgen05(mix):
-    tm = kernels(mix, "fused_persist_kernel", "ELi9ELi1E")  # TM = 1
+    tm = kernels(mix, "fused_persist_kernel", "ELi9ELi1E")  # TM = 1 (variant 23, n >= 256)
     assert len(tm) >= 2
     for f, c in tm.items():
         assert c["LDTM"] >= 1 and c["STTM"] >= 1 and c["UTCATOMSWS"] >= 1, f
+        assert c["UTMALDG"] >= 1 and c["SYNCS"] >= 10 and c["DFMA"] > 500, f
 
 
 def test_no_legacy_tensor_core_or_hopper_instructions(mix):

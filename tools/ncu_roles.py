@@ -76,10 +76,13 @@ def main():
     ix = {h: i for i, h in enumerate(hdr)}
     if len(sys.argv) > 5:
         mangled = sys.argv[5]
-    else:  # the default K_A / K_B kernel names of the product library
-        kb = "1" if "(int)1," in kname else "0"
-        mangled = ("_ZN3prk20fused_persist_kernelILi%sENS_9FusedCfgPILi16ELi9ELi4ELi2ELi2ELi2ELi2ELi0ELi9ELi0ELi0EEEEE"
-                   "vNS_11StencilArgsENS_7TmaMapsE" % kb)
+    else:  # fused_persist_kernel<KB, FusedCfgP<...>> of the product library, from ncu's name
+        m = re.search(r"fused_persist_kernel<\(int\)(\d+), prk::FusedCfgP<([^>]*)>>", kname)
+        if not m:
+            sys.exit("pass the mangled kernel name for " + kname)
+        args = "".join("Li%sE" % v for v in re.findall(r"\(int\)(-?\d+)", m.group(2)))
+        mangled = ("_ZN3prk20fused_persist_kernelILi%sENS_9FusedCfgPI%sEEEEvNS_11StencilArgsENS_7TmaMapsE"
+                   % (m.group(1), args))
     info = sass_chains(lib, mangled)
 
     def val(r, h):
