@@ -357,6 +357,10 @@ using FusedT32 = FusedCfgP<32, 7, 4, 4, 4, 2, 2, 0, 7>;
 using FusedT32B = FusedCfgP<32, 5, 3, 4, 4, 2, 2, 0, 5>;  // K_B at 32x32: shallower rings to fit
 // 32x16 tile with the stage A -> stage B per-point hand-off through tensor memory
 using FusedTM = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 1>;
+// the same with stage A's TMEM stores issued before its shared ones (PR_FTILE=38), or stage
+// B's three TMEM loads of an iteration behind one wait (39; spills), PRK_VARIANTS
+using FusedTM2 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 2>;
+using FusedTM3 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 3>;
 // timing diagnostics (garbage results): no input waits / no waits at all (PR_FTILE 26 / 27)
 using FusedD1 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 0, 1>;
 using FusedD2 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 0, 2>;
@@ -761,12 +765,16 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                             t0v[r].x = ac.x + (dt / 3.0) * k[r].x;
                             t0v[r].y = ac.y + (dt / 3.0) * k[r].y;
                         }
-                        sts2(zs + sZ + r * EW, zz[r]);  // x/y neighbours for stage B
+                        if constexpr (C::TM != 2) sts2(zs + sZ + r * EW, zz[r]);  // x/y neighbours for stage B
                     }
                     const uint32_t col = tq_addr + uint32_t(zpos.slot() * C::TM_PLANE);
                     tm_st8(col, zz[0], zz[1]);
                     tm_st8(col + 8, t0v[0], t0v[1]);
                     if (KB == K_A) tm_st8(col + 16, q[0][(P + 2) % 5], q[1][(P + 2) % 5]);
+                    if constexpr (C::TM == 2) {  // the shared stores under the TMEM stores' latency
+#pragma unroll
+                        for (int r = 0; r < RPT; ++r) sts2(zs + sZ + r * EW, zz[r]);
+                    }
                     tm_wait_st();
                     tm_fence_before();
                 } else if (valid) {
@@ -886,10 +894,16 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
         rotating_loop(NJ, [&](auto ph, int j) {
             constexpr int P = decltype(ph)::value;
             if (C::DIAG != 2 && !(C::SW && full_ok)) mbar_wait(full_s[zq_pos.slot()], zq_pos.round() & 1);
+            TmRaw8 tt0, tt1;  // TM: t0 and u of the output point (plane j-2)
             if constexpr (C::TM) {
                 tm_fence_after();
                 TmRaw8 tz;
                 tm_ld8(tq_addr + uint32_t(zq_pos.slot() * C::TM_PLANE), tz);  // own centre, plane j
+                if (C::TM == 3 && j >= 4) {  // TM 3: plane j-2's per-point values in the same wait
+                    const uint32_t cc = tq_addr + uint32_t(zc_pos.slot() * C::TM_PLANE);
+                    tm_ld8(cc + 8, tt0);
+                    if (KB == K_A) tm_ld8(cc + 16, tt1);
+                }
                 tm_wait_ld();
 #pragma unroll
                 for (int r = 0; r < RPT; ++r) q[r][(P + 4) % 5] = tm_row(tz, r);
@@ -914,8 +928,7 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
                 for (int r = 0; r < RPT; ++r)
                     kBs[r] = apply_pair<P>(W, lds2(zc + r * EW - 2), lds2(zc + r * EW + 2), col[r], col[r + 1],
                                            col[r + 3], col[r + 4], q[r]);
-                TmRaw8 tt0, tt1;  // TM: t0 and u of the output point (plane j-2)
-                if constexpr (C::TM) {
+                if constexpr (C::TM == 1 || C::TM == 2) {
                     const uint32_t cc = tq_addr + uint32_t(zc_pos.slot() * C::TM_PLANE);
                     tm_ld8(cc + 8, tt0);
                     if (KB == K_A) tm_ld8(cc + 16, tt1);
