@@ -555,8 +555,13 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": ("fused_persist_kernel<K_A>+<K_B>: one RK4 step = 2 launches "
-                                    "(stages 1+2, 3+4)") if fused else
-                                   "stencil_kernel<1..4>: one RK4 step = 4 launches",
+                                    "(stages 1+2, 3+4), design PR_FTILE=%d (%s)"
+                                    % (info["fine_variant"],
+                                       "per-point stage hand-off through tensor memory"
+                                       if info["fine_variant"] == 23 else
+                                       "per-point stage hand-off through shared memory"
+                                       if info["fine_variant"] == 14 else "alternative design"))
+                                   if fused else "stencil_kernel<1..4>: one RK4 step = 4 launches",
                          "launch": "one RK4 step of F (all its kernels), CUDA events on the launching "
                                    "stream around the fine phase of every timed solve",
                          "algorithmic_bytes_per_launch": impl_bytes * n ** 3,

@@ -247,12 +247,17 @@ pr_status pr_last_timings(pr_grid *grid, double *out, int32_t cap);
  *                          4 (one fused pass per RK4 stage);
  *   fine_bytes_per_point:  HBM bytes per grid point per RK4 step that path must
  *                          move (56, 16 or 128);
- *   coarse_bytes_per_point: 16 (one Euler pass). */
+ *   coarse_bytes_per_point: 16 (one Euler pass);
+ *   sms: streaming multiprocessors of the grid's device;
+ *   fine_variant:          the two-kernel F design in use, PR_FTILE numbering (14 per-point
+ *                          hand-off through shared memory, 23 through tensor memory, 22 / 24 /
+ *                          25 the alternatives of pr_fine), 0 on the four-pass path. */
 typedef struct {
     int32_t fine_kernels_per_step;
     int32_t fine_bytes_per_point;
     int32_t coarse_bytes_per_point;
     int32_t sms;
+    int32_t fine_variant;
 } pr_grid_info_t;
 pr_status pr_grid_info(const pr_grid *grid, pr_grid_info_t *info);
 

@@ -49,7 +49,8 @@ class PrOp(ctypes.Structure):
 
 class PrGridInfo(ctypes.Structure):
     _fields_ = [("fine_kernels_per_step", ctypes.c_int32), ("fine_bytes_per_point", ctypes.c_int32),
-                ("coarse_bytes_per_point", ctypes.c_int32), ("sms", ctypes.c_int32)]
+                ("coarse_bytes_per_point", ctypes.c_int32), ("sms", ctypes.c_int32),
+                ("fine_variant", ctypes.c_int32)]
 
 
 class PrError(RuntimeError):

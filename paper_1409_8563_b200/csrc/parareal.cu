@@ -2065,6 +2065,7 @@ pr_status pr_grid_info(const pr_grid *g, pr_grid_info_t *info) {
     info->fine_bytes_per_point = g->f1 ? 16 : g->f2 ? 56 : 128;
     info->coarse_bytes_per_point = 16;
     info->sms = g->sms;
+    info->fine_variant = g->f2 ? g->fvariant : 0;
     return PR_OK;
 }
 

@@ -234,6 +234,21 @@ def test_fine_paths_agree(n, f2, monkeypatch):
     g.destroy()
 
 
+def test_default_fine_design_per_size(monkeypatch):
+    """pr_grid_info names the two-kernel F design in use: the tensor-memory stage hand-off
+    (23) from 256^3 up, the shared-memory one (14) below, PR_FTILE overriding both, 0 on the
+    four-pass path (n not a multiple of 32)."""
+    monkeypatch.delenv("PR_FTILE", raising=False)
+    for n, want in ((128, 14), (256, 23), (40, 0)):
+        g = pr.Grid(pr.Problem(n, c=PARITY_C))
+        assert pr.pr_grid_info(g)["fine_variant"] == want, n
+        g.destroy()
+    monkeypatch.setenv("PR_FTILE", "14")
+    g = pr.Grid(pr.Problem(256, c=PARITY_C))
+    assert pr.pr_grid_info(g)["fine_variant"] == 14
+    g.destroy()
+
+
 @pytest.mark.parametrize("variant", [str(v) for v in list(range(10, 26)) + [29, 31, 32, 33, 34, 35, 36, 37, 38, 39]])
 def test_fused_variants_bitwise(variant, monkeypatch):
     """Every persistent fused tile variant (PR_FTILE) gives the four-stage
