@@ -32,7 +32,7 @@ template <int TYO_, int DEPTH_, int PW_ = 2, int FILL_ = 2, int ZD_ = 4>
 struct CombCfg {
     static constexpr bool COMB = true, Z2 = false, WP = false;
     static constexpr int DIAG = 0;
-    static constexpr bool PIN = false;
+    static constexpr bool PIN = true;
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, PW = PW_, FILL = FILL_;
     static constexpr int RPT = 2, RPTA = 2, XP = 2;
     static constexpr int EW = TXO + 4, EH = TYO + 4, IW = TXO + 8, IH = TYO + 8;
@@ -63,7 +63,10 @@ __device__ __forceinline__ void comb_consumer(const StencilArgs &a, double *sm, 
                                               uint64_t *in_full, uint64_t *in_empty, uint64_t *zfull,
                                               uint64_t *zempty) {
     constexpr int RPT = C::RPT, DEPTH = C::DEPTH, EW = C::EWS, IW = C::IWS, TXO = C::TXO, ZD = C::ZD;
-    double *yring = sm;
+    // barrier and ring addresses pinned in registers (fused.cuh, FusedCfgP::PIN)
+    const SBars zfull_s = sbars<C>(zfull), zempty_s = sbars<C>(zempty);
+    const SBars in_full_s = sbars<C>(in_full), in_empty_s = sbars<C>(in_empty);
+    double *yring = smem_base<C>(sm);
     double *aring = yring + size_t(DEPTH) * C::Y_ELEMS;
     double *zring = aring + (KB == K_B ? size_t(C::AD) * C::AUX_ELEMS : 0);
     const int t = threadIdx.x;
@@ -122,14 +125,14 @@ __device__ __forceinline__ void comb_consumer(const StencilArgs &a, double *sm, 
         RingPos p0 = base;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            mbar_wait(&in_full[p0.slot], p0.round & 1);
+            mbar_wait(in_full_s[p0.slot], p0.round & 1);
             const double *ys = yring + size_t(p0.slot) * C::Y_ELEMS + sY;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) qa[r][e] = lds2(ys + r * IW);
             p0.step(DEPTH);
         }
-        mbar_arrive(&in_empty[base.slot]);
-        mbar_arrive(&in_empty[ring_at(base, 1, DEPTH).slot]);
+        mbar_arrive(in_empty_s[base.slot]);
+        mbar_arrive(in_empty_s[ring_at(base, 1, DEPTH).slot]);
         RingPos p2 = ring_at(base, 2, DEPTH), p4 = p0;  // elements j+2, j+4
         RingPos zr = zw;  // intermediate ring: plane j-3 (stage B's centre in iteration j >= 5)
 
@@ -171,8 +174,8 @@ __device__ __forceinline__ void comb_consumer(const StencilArgs &a, double *sm, 
         // stage A results: the intermediate plane j (ring and own queue) and t0
         auto a_store = [&](auto ph, const ALd &L, const K2 &K) {
             constexpr int P = decltype(ph)::value;
-            mbar_arrive(&in_empty[p2.slot]);  // element j+2 done (aux j lives in slot j+4)
-            if (zw.round > 0) mbar_wait(&zempty[zw.slot], (zw.round - 1) & 1);
+            mbar_arrive(in_empty_s[p2.slot]);  // element j+2 done (aux j lives in slot j+4)
+            if (zw.round > 0) mbar_wait(zempty_s[zw.slot], (zw.round - 1) & 1);
             double *zd = zring + size_t(zw.slot) * C::Z_ELEMS + sZ;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) {
@@ -193,7 +196,7 @@ __device__ __forceinline__ void comb_consumer(const StencilArgs &a, double *sm, 
                 qb[r][P] = z;  // plane j replaces plane j-5
                 tq[r][P] = t0;
             }
-            mbar_arrive(&zfull[zw.slot]);
+            mbar_arrive(zfull_s[zw.slot]);
             zw.step(ZD);
             p2.step(DEPTH);
             p4.step(DEPTH);
@@ -244,19 +247,19 @@ __device__ __forceinline__ void comb_consumer(const StencilArgs &a, double *sm, 
             }
             o0 += nn;
             if (KB == K_A) o1 += nn;
-            mbar_arrive(&zempty[zr.slot]);  // plane j-3 read
+            mbar_arrive(zempty_s[zr.slot]);  // plane j-3 read
             zr.step(ZD);
         };
         // release a plane stage B never reads (0, 1, NJ-2, NJ-1) -- only once every lane has
         // written it: an early release could complete the slot's empty phase twice before
         // a slow writer waits on it (its parity wait would then never return)
         auto release_unread = [&]() {
-            mbar_wait(&zfull[zr.slot], zr.round & 1);
-            mbar_arrive(&zempty[zr.slot]);
+            mbar_wait(zfull_s[zr.slot], zr.round & 1);
+            mbar_arrive(zempty_s[zr.slot]);
             zr.step(ZD);
         };
         auto stage_a = [&](auto ph) {
-            mbar_wait(&in_full[p4.slot], p4.round & 1);  // element j+4 (+ aux j) landed
+            mbar_wait(in_full_s[p4.slot], p4.round & 1);  // element j+4 (+ aux j) landed
             ALd L;
             K2 K;
             a_load(ph, L);
@@ -264,7 +267,7 @@ __device__ __forceinline__ void comb_consumer(const StencilArgs &a, double *sm, 
             a_store(ph, L, K);
         };
         auto stage_b = [&](auto ph) {
-            mbar_wait(&zfull[zr.slot], zr.round & 1);
+            mbar_wait(zfull_s[zr.slot], zr.round & 1);
             BLd L;
             K2 K;
             b_load(ph, L);
@@ -284,8 +287,8 @@ __device__ __forceinline__ void comb_consumer(const StencilArgs &a, double *sm, 
             // j = 5 .. NJ-1: both stages; every wait first, then both stages' loads, so the
             // two dependency chains of the iteration overlap
             rotating_loop(NJ - 5, [&](auto ph, int) {
-                mbar_wait(&zfull[zr.slot], zr.round & 1);
-                mbar_wait(&in_full[p4.slot], p4.round & 1);
+                mbar_wait(zfull_s[zr.slot], zr.round & 1);
+                mbar_wait(in_full_s[p4.slot], p4.round & 1);
                 BLd LB;
                 ALd LA;
                 K2 KB_, KA_;
@@ -311,8 +314,8 @@ __device__ __forceinline__ void comb_consumer(const StencilArgs &a, double *sm, 
             rotating_loop(NJ, [&](auto ph, int) { stage_a(ph); });
         }
         // the item's last two input elements were only used by the queue
-        mbar_arrive(&in_empty[p2.slot]);
-        mbar_arrive(&in_empty[ring_at(p2, 1, DEPTH).slot]);
+        mbar_arrive(in_empty_s[p2.slot]);
+        mbar_arrive(in_empty_s[ring_at(p2, 1, DEPTH).slot]);
         base = ring_at(p2, 2, DEPTH);
     }
 }

@@ -46,7 +46,10 @@ __device__ __forceinline__ void stage_a_z2(const StencilArgs &a, double *sm, int
     constexpr int RPT = C::RPTA, DEPTH = C::template DEPTH_K<KB>, EW = C::EWS, IW = C::IWS, TXO = C::TXO,
                   ZD = C::ZD;
     constexpr int ZS = C::template ZS_ELEMS<KB>;
-    double *yring = sm;
+    // barrier and ring addresses pinned in registers (fused.cuh, FusedCfgP::PIN)
+    const SBars full_s = sbars<C>(full), empty_s = sbars<C>(empty);
+    const SBars in_full_s = sbars<C>(in_full), in_empty_s = sbars<C>(in_empty);
+    double *yring = smem_base<C>(sm);
     double *aring = yring + size_t(DEPTH) * C::Y_ELEMS;
     double *zring = aring + (KB == K_B ? size_t(C::AD) * C::AUX_ELEMS : 0);
     const int t = threadIdx.x;
@@ -78,14 +81,14 @@ __device__ __forceinline__ void stage_a_z2(const StencilArgs &a, double *sm, int
         RingPos p0 = base;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            mbar_wait(&in_full[p0.slot], p0.round & 1);
+            mbar_wait(in_full_s[p0.slot], p0.round & 1);
             const double *ys = yring + size_t(p0.slot) * C::Y_ELEMS + sY;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) q[r][e] = lds2(ys + r * IW);
             p0.step(DEPTH);
         }
-        mbar_arrive(&in_empty[base.slot]);
-        mbar_arrive(&in_empty[ring_at(base, 1, DEPTH).slot]);
+        mbar_arrive(in_empty_s[base.slot]);
+        mbar_arrive(in_empty_s[ring_at(base, 1, DEPTH).slot]);
         RingPos p2 = ring_at(base, 2, DEPTH), p4 = p0;  // elements j+2, j+4 (j = 2 jj)
         rotating_loop_by3(NJ / 2, [&](auto ph, int jj) {
             constexpr int B = 2 * decltype(ph)::value;  // index of element j
@@ -93,8 +96,8 @@ __device__ __forceinline__ void stage_a_z2(const StencilArgs &a, double *sm, int
             RingPos p3 = p2, p5 = p4;
             p3.step(DEPTH);
             p5.step(DEPTH);
-            mbar_wait(&in_full[p4.slot], p4.round & 1);
-            mbar_wait(&in_full[p5.slot], p5.round & 1);
+            mbar_wait(in_full_s[p4.slot], p4.round & 1);
+            mbar_wait(in_full_s[p5.slot], p5.round & 1);
             const double *yq4 = yring + size_t(p4.slot) * C::Y_ELEMS + sY;
             const double *yq5 = yring + size_t(p5.slot) * C::Y_ELEMS + sY;
 #pragma unroll
@@ -132,7 +135,7 @@ __device__ __forceinline__ void stage_a_z2(const StencilArgs &a, double *sm, int
             }
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                if (zpos.round > 0) mbar_wait(&empty[zpos.slot], (zpos.round - 1) & 1);
+                if (zpos.round > 0) mbar_wait(empty_s[zpos.slot], (zpos.round - 1) & 1);
                 double *zs = zring + size_t(zpos.slot) * ZS;
                 const bool outp = j + h >= 2 && j + h < w.nz + 2;
                 if (valid) {
@@ -167,18 +170,18 @@ __device__ __forceinline__ void stage_a_z2(const StencilArgs &a, double *sm, int
                         }
                     }
                 }
-                mbar_arrive(&full[zpos.slot]);
+                mbar_arrive(full_s[zpos.slot]);
                 zpos.step(ZD);
             }
-            mbar_arrive(&in_empty[p2.slot]);  // elements j+2, j+3 done
-            mbar_arrive(&in_empty[p3.slot]);
+            mbar_arrive(in_empty_s[p2.slot]);  // elements j+2, j+3 done
+            mbar_arrive(in_empty_s[p3.slot]);
             p2.step(DEPTH);
             p2.step(DEPTH);
             p4.step(DEPTH);
             p4.step(DEPTH);
         });
-        mbar_arrive(&in_empty[p2.slot]);
-        mbar_arrive(&in_empty[ring_at(p2, 1, DEPTH).slot]);
+        mbar_arrive(in_empty_s[p2.slot]);
+        mbar_arrive(in_empty_s[ring_at(p2, 1, DEPTH).slot]);
         base = ring_at(p2, 2, DEPTH);
     }
 }
@@ -188,6 +191,8 @@ __device__ __forceinline__ void stage_b_z2(const StencilArgs &a, double *sm, int
                                            uint64_t *empty) {
     constexpr int RPT = C::RPT, EW = C::EWS, TXO = C::TXO, ZD = C::ZD, DEPTH = C::template DEPTH_K<KB>;
     constexpr int ZS = C::template ZS_ELEMS<KB>;
+    const SBars full_s = sbars<C>(full), empty_s = sbars<C>(empty);
+    sm = smem_base<C>(sm);
     double *zring = sm + size_t(DEPTH) * C::Y_ELEMS + (KB == K_B ? size_t(C::AD) * C::AUX_ELEMS : 0);
     const int n = a.n;
     const size_t nn = size_t(n) * n;
@@ -220,8 +225,8 @@ __device__ __forceinline__ void stage_b_z2(const StencilArgs &a, double *sm, int
             constexpr int B = 2 * decltype(ph)::value;  // index of plane j
             RingPos zq1 = zq_pos;
             zq1.step(ZD);
-            mbar_wait(&full[zq_pos.slot], zq_pos.round & 1);
-            mbar_wait(&full[zq1.slot], zq1.round & 1);
+            mbar_wait(full_s[zq_pos.slot], zq_pos.round & 1);
+            mbar_wait(full_s[zq1.slot], zq1.round & 1);
             const double *zq[2] = {zring + size_t(zq_pos.slot) * ZS + sZ, zring + size_t(zq1.slot) * ZS + sZ};
 #pragma unroll
             for (int r = 0; r < RPT; ++r) {
@@ -274,18 +279,18 @@ __device__ __forceinline__ void stage_b_z2(const StencilArgs &a, double *sm, int
                 }
             }
             if (jj >= 1) {  // planes j-2 and j-1 are no longer read
-                mbar_arrive(&empty[zc_pos.slot]);
+                mbar_arrive(empty_s[zc_pos.slot]);
                 zc_pos.step(ZD);
-                mbar_arrive(&empty[zc_pos.slot]);
+                mbar_arrive(empty_s[zc_pos.slot]);
                 zc_pos.step(ZD);
             }
             zq_pos.step(ZD);
             zq_pos.step(ZD);
         });
         // the item's last two planes (never a centre)
-        mbar_arrive(&empty[zc_pos.slot]);
+        mbar_arrive(empty_s[zc_pos.slot]);
         zc_pos.step(ZD);
-        mbar_arrive(&empty[zc_pos.slot]);
+        mbar_arrive(empty_s[zc_pos.slot]);
     }
 }
 

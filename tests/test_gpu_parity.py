@@ -234,6 +234,26 @@ def test_fine_paths_agree(n, f2, monkeypatch):
     g.destroy()
 
 
+@pytest.mark.parametrize("n", [256])
+def test_default_designs_bitwise_at_256(n, monkeypatch):
+    """At the bench's size the two default designs (14 below 256^3, 23 from 256^3) and the
+    four-stage path give the same bits over a few RK4 steps."""
+    u0 = dev(random_field(n, 37))
+    outs = []
+    for f2, v in (("0", None), ("1", "14"), ("1", "23")):
+        monkeypatch.setenv("PR_F2", f2)
+        if v is None:
+            monkeypatch.delenv("PR_FTILE", raising=False)
+        else:
+            monkeypatch.setenv("PR_FTILE", v)
+        g = pr.Grid(pr.Problem(n, c=PARITY_C))
+        out = torch.empty_like(u0)
+        pr.pr_fine(g, u0, out, 3, 5, 1e-4 * (128 / n) ** 2)
+        outs.append(out)
+        g.destroy()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+
+
 def test_default_fine_design_per_size(monkeypatch):
     """pr_grid_info names the two-kernel F design in use: the tensor-memory stage hand-off
     (23) from 256^3 up, the shared-memory one (14) below, PR_FTILE overriding both, 0 on the
@@ -257,9 +277,12 @@ def test_fused_variants_bitwise(variant, monkeypatch):
     n = 128
     u0 = dev(random_field(n, 31))
     outs = []
-    for f2, v in (("0", "13"), ("1", variant)):
+    for f2, v in (("0", None), ("1", variant)):
         monkeypatch.setenv("PR_F2", f2)
-        monkeypatch.setenv("PR_FTILE", v)
+        if v is None:  # the four-stage path (no fused variant involved)
+            monkeypatch.delenv("PR_FTILE", raising=False)
+        else:
+            monkeypatch.setenv("PR_FTILE", v)
         try:
             g = pr.Grid(pr.Problem(n, c=PARITY_C))
         except pr.PrError as e:  # a tuning variant not built (PRK_VARIANTS) or not fitting
