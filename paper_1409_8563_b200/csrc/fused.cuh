@@ -361,6 +361,9 @@ using FusedTM = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 1>;
 // B's three TMEM loads of an iteration behind one wait (39; spills), PRK_VARIANTS
 using FusedTM2 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 2>;
 using FusedTM3 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 3>;
+// TMEM hand-off with a 16-slot K_A input ring (K_A has the shared memory to spare once the
+// per-point values leave the Z ring; PR_FTILE=42 with FusedTM for K_B, PRK_VARIANTS)
+using FusedTMQ16 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 16, 1>;
 // timing diagnostics (garbage results): no input waits / no waits at all (PR_FTILE 26 / 27)
 using FusedD1 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 0, 1>;
 using FusedD2 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 0, 2>;
