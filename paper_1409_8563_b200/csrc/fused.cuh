@@ -136,6 +136,13 @@ __device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap *map, 
                                           uint64_t *bar) {
     tma_load3(dst, map, x, y, z, smem_u32(bar));
 }
+// prefetch a 3-D tensor tile into L2 (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch3(const CUtensorMap *map, int x, int y, int z) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y), "r"(z)
+                 : "memory");
+}
 // Tensor maps of the TMA fills (FusedCfgP::FILL == 2), 3-D (x, y, z) over the
 // n^3 fields, boxes one z plane deep: the padded smem pitch is the box width.
 struct TmaMaps {
@@ -292,6 +299,9 @@ struct FusedCfgP {
     // 2-3 % faster than letting the compiler rebuild them per iteration (variant 36 = off)
     static constexpr bool PIN = true;
     static constexpr bool OFF32 = false;  // stage-B stores by 32-bit element offsets (n^3 < 2^32)
+    // ACCG (with TM): K_B's stage B reads acc from global memory itself (LDG, the producer only
+    // prefetches the tile into L2), stage A hands k3 instead of t0 = acc + dt/3 k3 through TMEM
+    static constexpr bool ACCG = false;
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = 1, XP = 2,
                          PROD = 1, PW = PW_;  // PW producer warps
     // FILL 0: every plane by 16-byte cp.async; 2: planes of tiles away from the
@@ -364,6 +374,11 @@ using FusedTM3 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 3>;
 // TMEM hand-off with a 16-slot K_A input ring (K_A has the shared memory to spare once the
 // per-point values leave the Z ring; PR_FTILE=42 with FusedTM for K_B, PRK_VARIANTS)
 using FusedTMQ16 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 16, 1>;
+template <class C> struct WithACCG : C {
+    static_assert(C::TM == 1, "ACCG hands k3 through tensor memory");
+    static constexpr bool ACCG = true;
+};
+using FusedTMACC = WithACCG<FusedTM>;  // PR_FTILE=43 (PRK_VARIANTS)
 // timing diagnostics (garbage results): no input waits / no waits at all (PR_FTILE 26 / 27)
 using FusedD1 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 0, 1>;
 using FusedD2 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 0, 2>;
@@ -552,7 +567,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
                         const uint32_t bar = in_full_s[pos.slot()];
                         const int j = e - 4;
                         const bool ua = KB == K_B && j >= 0 && j < NJ;
-                        const bool ca = ua && j >= 2 && j < w.nz + 2;
+                        const bool ca = ua && j >= 2 && j < w.nz + 2 && !C::ACCG;
                         mbar_expect_tx(bar, 8u * (C::IH * IW + (ua ? C::EH * EW : 0) +
                                                   (ca ? C::T_ELEMS : 0)));
                         tma_load3(yring_s + uint32_t(pos.slot()) * (C::Y_ELEMS * 8), &tm->y,
@@ -562,6 +577,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
                             const uint32_t dst = aring_s + uint32_t(pos.slot()) * (C::AUX_ELEMS * 8);
                             tma_load3(dst, &tm->u, w.x0 - 2, w.y0 - 2, zaux, bar);
                             if (ca) tma_load3(dst + 8 * C::Z_ELEMS, &tm->c, w.x0, w.y0, zaux, bar);
+                            if (C::ACCG && j >= 2 && j < w.nz + 2) tma_prefetch3(&tm->c, w.x0, w.y0, zaux);
                         }
                     }
                     cp_async_mbar_arrive(in_full_s[pos.slot()]);
@@ -587,7 +603,7 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
 #pragma unroll
                     for (int k = 0; k < NU; ++k)
                         if (usrc[k] >= 0) cp_async16s(dst + udst[k], a.p0 + pl + usrc[k]);
-                    if (j >= 2 && j < w.nz + 2) {
+                    if (!C::ACCG && j >= 2 && j < w.nz + 2) {
 #pragma unroll
                         for (int k = 0; k < NC; ++k)
                             if (csrc[k] >= 0) cp_async16s(dst + cdst[k], a.p1 + pl + csrc[k]);
@@ -708,7 +724,7 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                     d.ub[r] = lds2(au + sZ + r * EW);
                     const int er = r0 + r;
                     const bool need = tcol && er >= 2 && er < C::TYO + 2;
-                    d.ac[r] = lds2(au + C::Z_ELEMS + (need ? tp0 + r * TXO : 0));
+                    if constexpr (!C::ACCG) d.ac[r] = lds2(au + C::Z_ELEMS + (need ? tp0 + r * TXO : 0));
                 }
             }
         };
@@ -762,11 +778,16 @@ __device__ __forceinline__ void stage_a_p(const StencilArgs &a, double *sm, int 
                             t0v[r].x = yc.x + (dt / 6.0) * k[r].x;
                             t0v[r].y = yc.y + (dt / 6.0) * k[r].y;
                         } else {
-                            const double2 ub = ubv[KB == K_B ? r : 0], ac = acv[KB == K_B ? r : 0];
+                            const double2 ub = ubv[KB == K_B ? r : 0];
                             zz[r].x = ub.x + dt * k[r].x;
                             zz[r].y = ub.y + dt * k[r].y;
-                            t0v[r].x = ac.x + (dt / 3.0) * k[r].x;
-                            t0v[r].y = ac.y + (dt / 3.0) * k[r].y;
+                            if constexpr (C::ACCG) {  // k3 itself: stage B adds acc
+                                t0v[r] = k[r];
+                            } else {
+                                const double2 ac = acv[KB == K_B ? r : 0];
+                                t0v[r].x = ac.x + (dt / 3.0) * k[r].x;
+                                t0v[r].y = ac.y + (dt / 3.0) * k[r].y;
+                            }
                         }
                         if constexpr (C::TM != 2) sts2(zs + sZ + r * EW, zz[r]);  // x/y neighbours for stage B
                     }
@@ -896,6 +917,13 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
         RingP<ZD> zc_pos = zq_pos;  // Z plane j-2 (valid from j = 2)
         rotating_loop(NJ, [&](auto ph, int j) {
             constexpr int P = decltype(ph)::value;
+            [[maybe_unused]] double2 accv[KB == K_B && C::ACCG ? RPT : 1];
+            if constexpr (KB == K_B && C::ACCG) {  // acc of this iteration's output points (j >= 4)
+                if (j >= 4 && valid) {
+#pragma unroll
+                    for (int r = 0; r < RPT; ++r) accv[r] = *reinterpret_cast<const double2 *>(o0 + size_t(r) * n);
+                }
+            }
             if (C::DIAG != 2 && !(C::SW && full_ok)) mbar_wait(full_s[zq_pos.slot()], zq_pos.round() & 1);
             TmRaw8 tt0, tt1;  // TM: t0 and u of the output point (plane j-2)
             if constexpr (C::TM) {
@@ -960,7 +988,12 @@ __device__ __forceinline__ void stage_b_p(const StencilArgs &a, double *sm, int 
                             *reinterpret_cast<double2 *>(o1 + gofs) = v1;
                         }
                     } else {
-                        const double2 t0 = C::TM ? tm_row(tt0, r) : lds2(zs + C::Z_ELEMS + sT + r * TXO);
+                        double2 t0 = C::TM ? tm_row(tt0, r) : lds2(zs + C::Z_ELEMS + sT + r * TXO);
+                        if constexpr (KB == K_B && C::ACCG) {  // t0 = acc + dt/3 k3, as stage A would
+                            const double2 k3 = t0;
+                            t0.x = accv[r].x + (dt / 3.0) * k3.x;
+                            t0.y = accv[r].y + (dt / 3.0) * k3.y;
+                        }
                         double2 v0;
                         v0.x = t0.x + (dt / 6.0) * kB.x;  v0.y = t0.y + (dt / 6.0) * kB.y;
                         if constexpr (C::OFF32) {
@@ -1016,6 +1049,7 @@ template <int TYO_, int DEPTH_, int RPT_, int PW_, int FILL_>
 struct CoarseCfgP {
     static constexpr int DIAG = 0;
     static constexpr bool PIN = false;
+    static constexpr bool ACCG = false;
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, RPT = RPT_, PW = PW_, FILL = FILL_;
     static constexpr int HX = 2, HY = 1, HZ = 1;  // radius-1 stencil; x halo pair-aligned
     static constexpr int IW = TXO + 2 * HX, IH = TYO + 2 * HY, IWS = IW;
