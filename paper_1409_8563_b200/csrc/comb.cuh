@@ -34,6 +34,7 @@ struct CombCfg {
     static constexpr int DIAG = 0;
     static constexpr bool PIN = true;
     static constexpr bool ACCG = false;
+    static constexpr int PFL2 = 0;
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, PW = PW_, FILL = FILL_;
     static constexpr int RPT = 2, RPTA = 2, XP = 2;
     static constexpr int EW = TXO + 4, EH = TYO + 4, IW = TXO + 8, IH = TYO + 8;

@@ -302,6 +302,9 @@ struct FusedCfgP {
     // ACCG (with TM): K_B's stage B reads acc from global memory itself (LDG, the producer only
     // prefetches the tile into L2), stage A hands k3 instead of t0 = acc + dt/3 k3 through TMEM
     static constexpr bool ACCG = false;
+    // PFL2 > 0: the producer also prefetches the input plane PFL2 planes ahead into L2
+    // (cp.async.bulk.prefetch.tensor), so the ring's TMA fills hit L2
+    static constexpr int PFL2 = 0;
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, ZD = ZD_, MINB = 1, XP = 2,
                          PROD = 1, PW = PW_;  // PW producer warps
     // FILL 0: every plane by 16-byte cp.async; 2: planes of tiles away from the
@@ -379,6 +382,9 @@ template <class C> struct WithACCG : C {
     static constexpr bool ACCG = true;
 };
 using FusedTMACC = WithACCG<FusedTM>;  // PR_FTILE=43 (PRK_VARIANTS)
+template <class C, int D> struct WithPFL2 : C { static constexpr int PFL2 = D; };
+using FusedTMPF4 = WithPFL2<FusedTM, 4>;  // PR_FTILE=44 (PRK_VARIANTS)
+using FusedTMPF8 = WithPFL2<FusedTM, 8>;  // PR_FTILE=45
 // timing diagnostics (garbage results): no input waits / no waits at all (PR_FTILE 26 / 27)
 using FusedD1 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 0, 1>;
 using FusedD2 = FusedCfgP<16, 9, 4, 2, 2, 2, 2, 0, 9, 0, 2>;
@@ -572,6 +578,13 @@ __device__ __forceinline__ void producer_p(const StencilArgs &a, const TmaMaps *
                                                   (ca ? C::T_ELEMS : 0)));
                         tma_load3(yring_s + uint32_t(pos.slot()) * (C::Y_ELEMS * 8), &tm->y,
                                   w.x0 - C::HX, w.y0 - C::HY, zin, bar);
+                        if constexpr (C::PFL2 > 0) {  // within this item's planes only
+                            if (e + C::PFL2 < E) {
+                                int zp = zin + C::PFL2;
+                                if (zp >= n) zp -= n;
+                                tma_prefetch3(&tm->y, w.x0 - C::HX, w.y0 - C::HY, zp);
+                            }
+                        }
                         if (ua) {
                             const int zaux = zin >= 2 ? zin - 2 : zin - 2 + n;
                             const uint32_t dst = aring_s + uint32_t(pos.slot()) * (C::AUX_ELEMS * 8);
@@ -1050,6 +1063,7 @@ struct CoarseCfgP {
     static constexpr int DIAG = 0;
     static constexpr bool PIN = false;
     static constexpr bool ACCG = false;
+    static constexpr int PFL2 = 0;
     static constexpr int TXO = 32, TYO = TYO_, DEPTH = DEPTH_, RPT = RPT_, PW = PW_, FILL = FILL_;
     static constexpr int HX = 2, HY = 1, HZ = 1;  // radius-1 stencil; x halo pair-aligned
     static constexpr int IW = TXO + 2 * HX, IH = TYO + 2 * HY, IWS = IW;

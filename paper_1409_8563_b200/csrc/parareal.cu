@@ -415,7 +415,8 @@ static void launch_coarse_persist(pr_grid *g, const StencilArgs &a0, cudaStream_
     X(26, FusedD1, FusedD1) X(27, FusedD2, FusedD2) X(28, FusedD3, FusedD3) X(31, FusedQ16, FusedQ16) \
     X(32, FusedQ8, FusedQ8) X(29, FusedPF, FusedPF) X(33, FusedZD6, FusedP5) X(34, FusedZD8, FusedP5) \
     X(35, FusedSW, FusedSW) X(36, FusedNoPIN, FusedNoPIN) X(37, FusedOFF32, FusedOFF32) X(38, FusedTM2, FusedTM2) X(39, FusedTM3, FusedTM3) \
-    X(40, FusedTM, FusedP4) X(41, FusedP4, FusedTM) X(42, FusedTMQ16, FusedTM) X(43, FusedTMACC, FusedTMACC)
+    X(40, FusedTM, FusedP4) X(41, FusedP4, FusedTM) X(42, FusedTMQ16, FusedTM) X(43, FusedTMACC, FusedTMACC) X(44, FusedTMPF4, FusedTMPF4) \
+    X(45, FusedTMPF8, FusedTMPF8)
 #else
 #define PRK_FVARIANTS_OLD(X)
 #endif

@@ -269,7 +269,7 @@ def test_default_fine_design_per_size(monkeypatch):
     g.destroy()
 
 
-@pytest.mark.parametrize("variant", [str(v) for v in list(range(10, 26)) + [29, 31, 32, 33, 34, 35, 36, 37, 38, 39, 40, 41, 42, 43]])
+@pytest.mark.parametrize("variant", [str(v) for v in list(range(10, 26)) + [29, 31, 32, 33, 34, 35, 36, 37, 38, 39, 40, 41, 42, 43, 44, 45]])
 def test_fused_variants_bitwise(variant, monkeypatch):
     """Every persistent fused tile variant (PR_FTILE) gives the four-stage
     path's bits: same folded weights, same operation order per point.  n = 128
